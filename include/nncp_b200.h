@@ -1,0 +1,144 @@
+/*
+ * nncp_b200.h -- C ABI of the B200-native dense NNCP hot path.
+ *
+ * Drop-in boundary for the reference package `nncp` (/root/reference/pkg/src/nncp),
+ * whose hot path is the alternating-update loop of driver.py:331-449.  Each entry
+ * point below replaces one numeric call site of that loop; the replaced reference
+ * interface is cited on every declaration.  The reference is pure Python, so the
+ * binding a maintainer adds is a ctypes stub (INTEGRATION.md shows it); this
+ * repository's own Python mirror (paper_1909_01149_b200/) binds exactly these
+ * symbols.
+ *
+ * Conventions (identical to the reference, tensor_ops.py:1-13):
+ *   - tensors: flat float64, mode-1 index fastest (column-major generalisation);
+ *   - factor matrices: row-major (I_n, R) float64;
+ *   - dimension-tree temporaries: retained-mode indices fastest, rank slowest
+ *     (dimtree.py:68-99), i.e. column-major (prod(retained), R);
+ *   - Gram buffers hold the RAW H^T H (R x R, row-major); every consumer reads the
+ *     symmetrised 0.5 (G + G^T) exactly as driver.py:353,422 stores it.
+ * All pointers are DEVICE pointers (caller-owned, e.g. torch CUDA tensors) unless
+ * the parameter is documented as host.  Every call is asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream) and returns NNCP_OK or an error
+ * code; nncp_last_error() returns the thread-local message.  Workspaces must be
+ * zero-filled once at allocation (they carry self-resetting reduction tickets).
+ */
+#ifndef NNCP_B200_H
+#define NNCP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNCP_ABI_VERSION 1
+#define NNCP_MAX_ORDER 8
+#define NNCP_MAX_RANK 64
+#define NNCP_STATUS_WORDS 4
+
+/* return codes; the Python mirror maps VALUE -> ValueError, RUNTIME -> RuntimeError */
+#define NNCP_OK 0
+#define NNCP_ERR_VALUE 1
+#define NNCP_ERR_RUNTIME 2
+#define NNCP_ERR_CUDA 3
+#define NNCP_ERR_UNSUPPORTED 4
+
+#define NNCP_SIDE_LEFT 0      /* dimtree.py:111-117: T = X_(1:S)   . KRP(H_{S+1..N}) */
+#define NNCP_SIDE_RIGHT 1     /* dimtree.py:118-124: T = X_(1:S)^T . KRP(H_{1..S})   */
+#define NNCP_TTV_TRAILING 0   /* dimtree.py:159-165 */
+#define NNCP_TTV_LEADING 1    /* dimtree.py:166-172 */
+#define NNCP_ALGO_MU 1        /* updaters.py:91-94   */
+#define NNCP_ALGO_HALS 2      /* updaters.py:97-118  */
+#define NNCP_ALGO_BPP 3       /* updaters.py:121-164 */
+
+/* status words (device int32[NNCP_STATUS_WORDS]) written by nncp_update:
+ *   [0],[1]  HALS: bit r set when gram diagonal r <= 0 (updaters.py:110-113)
+ *   [2]      BPP : smallest failing row, INT32_MAX when none (updaters.py:155,163)
+ *   [3]      BPP : failure kind, 0 none, 1 cycling (BppCyclingError), 2 singular solve
+ * The caller zero-fills [0],[1],[3] and sets [2]=INT32_MAX before the call
+ * (nncp_status_reset does it on the stream). */
+
+int nncp_abi_version(void);
+const char* nncp_last_error(void);
+/* SM count of the current device, for host-side bookkeeping */
+int nncp_device_sms(void);
+
+/* dimtree.py:25-39 choose_split_mode.  dims: host array. */
+int nncp_choose_split(int order, const int64_t* dims, int strict, int* split_out);
+
+/* Workspace bytes that covers every call below for this local tensor shape/rank. */
+size_t nncp_workspace_bytes(int order, const int64_t* dims, int split, int rank);
+
+/* tensor_ops.py:76-78 norm_squared: out[0] = sum x^2 (deterministic reduction). */
+int nncp_norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* dimtree.py:102-127 partial_mttkrp.  dims: host.  factors: host array of `order`
+ * device pointers (row-major (dims[n], R)); only the contracted side's factors are
+ * read.  out: column-major (prod(retained), R).  The Khatri-Rao rows are generated
+ * on the fly (never materialised); FP64 tensor cores (DMMA) fed by TMA. */
+int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int split, int side,
+                        const double* const* factors, int rank, double* out, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* dimtree.py:135-175 multi_ttv.  temp: column-major (prod(ret_dims), R).
+ * TRAILING: coeff = KRP(coeff[0..ncoeff)) with coeff_rows[k] rows each, whose
+ *   product must equal prod(ret_dims[1:]); out retains ret_dims[0].
+ * LEADING : ncoeff == 1, coeff[0] is (ret_dims[0], R); out retains ret_dims[1:].
+ * ret_dims, coeff, coeff_rows: host arrays. */
+int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, int side,
+                   const double* const* coeff, const int64_t* coeff_rows, int ncoeff, double* out,
+                   void* stream);
+
+/* dimtree.py:287 np.ascontiguousarray(temp.as_matrix()): column-major -> row-major. */
+int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_rows, void* stream);
+
+/* Status reset on the stream (see status words above). */
+int nncp_status_reset(int* status, void* stream);
+
+/* Fused NNLS factor update (driver.py:396-418 first half + updaters.py):
+ *   S = prod_{m != mode} sym(G_m)          (tensor_ops.py:146-155), or when order == 0
+ *       `grams` is S itself (R x R, used as given: UpdateInputs.gram);
+ *   current = owned * lam (lam may be NULL -> ones)                (driver.py:403);
+ *   hhat = MU / HALS / BPP(S, mttkrp_rows, current)                (updaters.py);
+ *   nsq[r] = sum_i hhat[i,r]^2 (may be NULL)                       (driver.py:413);
+ *   beta[0] = <mttkrp_rows, hhat> when beta != NULL                (driver.py:428).
+ * mttkrp_rows, owned, hhat: row-major (rows, R). */
+int nncp_update(int algo, const double* grams, int order, int mode, int rank,
+                const double* mttkrp_rows, const double* owned, const double* lam, int64_t rows,
+                double* hhat, double* nsq, double* beta, int* status, void* ws, size_t ws_bytes,
+                void* stream);
+
+/* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
+ * gram = owned^T owned (raw, local rows).  owned may alias hhat. */
+int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank,
+                        double* owned, double* lam, double* gram, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* driver.py:351 local Gram h^T h (raw). */
+int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, size_t ws_bytes,
+              void* stream);
+
+/* driver.py:368,431 gamma = lam^T (prod_m sym(G_m)) lam over all `order` Grams. */
+int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma,
+               void* stream);
+
+/* tensor_ops.py:208-212 matrix_inner_product <a, b * lam> (lam may be NULL). */
+int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank,
+               double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Synthetic input (BASELINE.json configs; tensor_io.py:103-125 generalised with noise):
+ * x[i] = sum_r prod_n H_n(i_n, r) + noise_scale * |N(0,1)|_i, the Gaussian drawn from
+ * Philox4x32-10 keyed by (seed) and counted by the GLOBAL linear index, so every grid
+ * block is bit-identical to the matching slice of the global tensor.
+ * local_dims/offsets/global_dims: host.  factors: host array of device pointers to the
+ * LOCAL row blocks (local_dims[n] x R). */
+int nncp_synthetic(double* x, int order, const int64_t* local_dims, const int64_t* offsets,
+                   const int64_t* global_dims, const double* const* factors, int rank,
+                   double noise_scale, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NNCP_B200_H */

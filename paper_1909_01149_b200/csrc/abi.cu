@@ -1,0 +1,156 @@
+// extern "C" boundary (include/nncp_b200.h): argument validation, error
+// reporting and dispatch to the kernels.  Validation messages mirror the
+// reference's ValueError / RuntimeError texts where one exists.
+#include <string>
+
+#include "common.cuh"
+
+namespace nncp {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+// kernels (defined in the other translation units)
+struct PartialPlan;
+int partial_mttkrp(const double*, int, const int64_t*, int, int, const double* const*, int, double*, void*, size_t,
+                   cudaStream_t);
+size_t partial_ws_bytes(int order, const int64_t* dims, int split, int side, int rank);
+int multi_ttv(const double*, int, const int64_t*, int, int, const double* const*, const int64_t*, int, double*,
+              cudaStream_t);
+int temp_to_rows(const double*, int64_t, int, double*, cudaStream_t);
+int update(int, const double*, int, int, int, const double*, const double*, const double*, int64_t, double*, double*,
+           double*, int*, void*, size_t, cudaStream_t);
+int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
+                   int);
+int gamma(const double*, int, int, const double*, double*, cudaStream_t);
+int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
+int norm_squared(const double*, int64_t, double*, void*, size_t, cudaStream_t);
+int status_reset(int*, cudaStream_t);
+size_t row_update_part_elems(int64_t rows, int rank);
+int synthetic(double*, int, const int64_t*, const int64_t*, const int64_t*, const double* const*, int, double,
+              uint64_t, cudaStream_t);
+
+static int check_common(int order, const int64_t* dims, int rank) {
+  if (order < 2 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "tensor order must be in [2, 8]");
+  if (rank < 1) return fail(NNCP_ERR_VALUE, "rank must be at least 1");
+  if (rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank above 64 is not supported on the device path");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return fail(NNCP_ERR_VALUE, "dims must be positive");
+  return NNCP_OK;
+}
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace nncp
+
+using namespace nncp;
+
+extern "C" {
+
+int nncp_abi_version(void) { return NNCP_ABI_VERSION; }
+const char* nncp_last_error(void) { return g_last_error.c_str(); }
+int nncp_device_sms(void) { return num_sms(); }
+
+int nncp_choose_split(int order, const int64_t* dims, int strict, int* split_out) {
+  if (order < 2) return fail(NNCP_ERR_VALUE, "need at least 2 modes");
+  for (int s = 1; s < order; ++s) {
+    // products can exceed int64 only for absurd shapes; use long double to compare safely
+    long double left = 1, right = 1;
+    for (int n = 0; n < s; ++n) left *= (long double)dims[n];
+    for (int n = s; n < order; ++n) right *= (long double)dims[n];
+    if (left > right || (!strict && left == right)) {
+      *split_out = s;
+      return NNCP_OK;
+    }
+  }
+  *split_out = order - 1;
+  return NNCP_OK;
+}
+
+size_t nncp_workspace_bytes(int order, const int64_t* dims, int split, int rank) {
+  size_t b = 0;
+  b = std::max(b, partial_ws_bytes(order, dims, split, NNCP_SIDE_LEFT, rank));
+  b = std::max(b, partial_ws_bytes(order, dims, split, NNCP_SIDE_RIGHT, rank));
+  int64_t maxrows = 1;
+  for (int n = 0; n < order; ++n) maxrows = std::max<int64_t>(maxrows, dims[n]);
+  b = std::max(b, 256 + sizeof(double) * row_update_part_elems(maxrows, rank));
+  return 256 + b;
+}
+
+int nncp_norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0) return fail(NNCP_ERR_VALUE, "negative length");
+  return norm_squared(x, n, out, ws, ws_bytes, S(stream));
+}
+
+int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int split, int side,
+                        const double* const* factors, int rank, double* out, void* ws, size_t ws_bytes,
+                        void* stream) {
+  int rc = check_common(order, dims, rank);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (side != NNCP_SIDE_LEFT && side != NNCP_SIDE_RIGHT)
+    return fail(NNCP_ERR_VALUE, "side must be 'left' or 'right'");
+  // the partial kernels use the first 256 bytes of nothing: split-K partials start at ws
+  return partial_mttkrp(x, order, dims, split, side, factors, rank, out, ws ? static_cast<char*>(ws) + 256 : nullptr,
+                        ws_bytes > 256 ? ws_bytes - 256 : 0, S(stream));
+}
+
+int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, int side,
+                   const double* const* coeff, const int64_t* coeff_rows, int ncoeff, double* out, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_VALUE, "bad rank");
+  return multi_ttv(temp, nret, ret_dims, rank, side, coeff, coeff_rows, ncoeff, out, S(stream));
+}
+
+int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_rows, void* stream) {
+  return temp_to_rows(temp, rows, rank, out_rows, S(stream));
+}
+
+int nncp_status_reset(int* status, void* stream) { return status_reset(status, S(stream)); }
+
+int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                int* status, void* ws, size_t ws_bytes, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
+  if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
+  if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
+  if (!status) return fail(NNCP_ERR_VALUE, "status buffer required");
+  return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
+                S(stream));
+}
+
+int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
+                        double* gram, void* ws, size_t ws_bytes, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  if (!nsq) return fail(NNCP_ERR_VALUE, "nsq required");
+  return normalize_gram(hhat, nsq, rows, rank, owned, lam, gram, ws, ws_bytes, S(stream), 2);
+}
+
+int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, size_t ws_bytes, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  return normalize_gram(h, nullptr, rows, rank, nullptr, nullptr, gram, ws, ws_bytes, S(stream), 3);
+}
+
+int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma_out, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  return gamma(grams, order, rank, lam, gamma_out, S(stream));
+}
+
+int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank, double* out, void* ws,
+               size_t ws_bytes, void* stream) {
+  return inner(a, b, lam, rows, rank, out, ws, ws_bytes, S(stream));
+}
+
+int nncp_synthetic(double* x, int order, const int64_t* local_dims, const int64_t* offsets,
+                   const int64_t* global_dims, const double* const* factors, int rank, double noise_scale,
+                   uint64_t seed, void* stream) {
+  int rc = check_common(order, local_dims, rank);
+  if (rc) return rc;
+  return synthetic(x, order, local_dims, offsets, global_dims, factors, rank, noise_scale, seed, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,613 @@
+// Normal-equation side of the ALS step: Hadamard-of-Grams, MU / HALS / ANLS-BPP
+// row updates, column norms, normalisation, Gram matrices, error terms.
+// References: tensor_ops.py:140-155, updaters.py:91-164, driver.py:396-433.
+//
+// Every factor row is an independent NNLS problem (updaters.py:1-8), so the
+// updates run one thread (MU, HALS) or one warp (BPP) per row with S = A^T A
+// staged once per CTA in shared memory.  Column sums (norms, beta, Grams) use
+// per-CTA partials plus a last-CTA fixed-order reduction: deterministic and a
+// single launch.
+#include <climits>
+
+#include "common.cuh"
+
+namespace nncp {
+
+// --------------------------------------------------------------- helpers --
+// S[a][b] = prod_{m != mode} 0.5 (G_m[a][b] + G_m[b][a]); order==0: S = grams.
+__device__ void load_hadamard(double* S, const double* __restrict__ grams, int order, int mode, int R) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    double v;
+    if (order == 0) {
+      v = grams[e];
+    } else {
+      v = 1.0;
+      for (int m = 0; m < order; ++m) {
+        if (m == mode) continue;
+        const double* g = grams + size_t(m) * R * R;
+        v *= 0.5 * (g[a * R + b] + g[b * R + a]);
+      }
+    }
+    S[e] = v;
+  }
+}
+
+__device__ double block_sum(double v, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    s = red[0];
+    for (int w = 1; w < nw; ++w) s += red[w];
+  }
+  __syncthreads();
+  return s;
+}
+
+// Final fixed-order reduction of per-CTA partials [nblk][n] -> out[n] by the last CTA.
+__device__ void finish_partials(const double* part, int nblk, int n, double* out) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    double s = part[e];
+    for (int b = 1; b < nblk; ++b) s += part[size_t(b) * n + e];
+    out[e] = s;
+  }
+}
+
+// Workspace carve-up (bytes): [0,256) tickets, then partial buffers.
+struct WsLayout {
+  unsigned int* tickets;
+  double* part;
+  size_t part_elems;
+};
+inline WsLayout ws_layout(void* ws, size_t bytes) {
+  WsLayout w;
+  w.tickets = static_cast<unsigned int*>(ws);
+  w.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  w.part_elems = bytes > 256 ? (bytes - 256) / sizeof(double) : 0;
+  return w;
+}
+enum Ticket { T_NORM = 0, T_UPDATE = 1, T_NORMGRAM = 2, T_GRAM = 3, T_INNER = 4 };
+
+// ------------------------------------------------------------ MU / HALS ----
+// One warp per row; lane l holds columns l and l+32 (R <= 64).
+constexpr int kRowWarps = 8;
+
+// Per-CTA column sums of squares (+ beta) -> partials, last CTA reduces in order.
+template <int NH>
+__device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, double* red /* [nw][64] */,
+                                double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NH; ++q) red[warp * 64 + lane + 32 * q] = sq[q];
+  __syncthreads();
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double s = red[r];
+    for (int w = 1; w < nw; ++w) s += red[w * 64 + r];
+    colbuf[r] = s;
+  }
+  __syncthreads();
+  if (beta) {
+    const double b = block_sum(bsum, red);
+    if (threadIdx.x == 0) colbuf[R] = b;
+    __syncthreads();
+  }
+  const int stride = R + 1;
+  for (int e = threadIdx.x; e < stride; e += blockDim.x) part[size_t(blockIdx.x) * stride + e] = colbuf[e];
+  if (last_cta_ticket(ticket)) {
+    const int nblk = gridDim.x;
+    for (int e = threadIdx.x; e < stride; e += blockDim.x) {
+      if (e == R && !beta) continue;
+      double s = part[e];
+      for (int b = 1; b < nblk; ++b) s += part[size_t(b) * stride + e];
+      if (e < R) {
+        if (nsq) nsq[e] = s;
+      } else {
+        beta[0] = s;
+      }
+    }
+  }
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(kRowWarps * 32)
+    update_rows_kernel(const double* __restrict__ grams, int order, int mode, int R,
+                       const double* __restrict__ mrows, const double* __restrict__ owned,
+                       const double* __restrict__ lam, int64_t rows, double* __restrict__ hhat,
+                       double* __restrict__ part, double* nsq, double* beta, int* status, unsigned int* ticket) {
+  __shared__ double S[kMaxRank * kMaxRank];
+  __shared__ double red[kRowWarps * 64];
+  __shared__ double colbuf[kMaxRank + 1];
+  load_hadamard(S, grams, order, mode, R);
+  __syncthreads();
+  if (ALGO == NNCP_ALGO_HALS && blockIdx.x == 0) {
+    for (int r = threadIdx.x; r < R; r += blockDim.x)
+      if (S[r * R + r] <= 0.0) atomicOr(status + (r >> 5), int(1u << (r & 31)));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double sq[2] = {0.0, 0.0};
+  double bsum = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kRowWarps + warp; i < rows; i += int64_t(gridDim.x) * kRowWarps) {
+    const double* orow = owned + i * R;
+    const double* mr = mrows + i * R;
+    double h[2], m[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = lane + 32 * q;
+      h[q] = (r < R) ? (lam ? orow[r] * lam[r] : orow[r]) : 0.0;  // driver.py:403 current = owned * lam
+      m[q] = (r < R) ? mr[r] : 0.0;
+    }
+    if (ALGO == NNCP_ALGO_MU) {
+      // updaters.py:93-94: current * M / (current @ S + eps)
+      double d[2] = {0.0, 0.0};
+      for (int cc = 0; cc < R; ++cc) {
+        const double hc = __shfl_sync(0xffffffffu, cc < 32 ? h[0] : h[1], cc & 31);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = lane + 32 * q;
+          if (r < R) d[q] = fma(hc, S[cc * R + r], d[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = lane + 32 * q;
+        h[q] = (r < R) ? h[q] * m[q] / (d[q] + 1e-16) : 0.0;
+      }
+    } else {
+      // updaters.py:107-118: Gauss-Seidel over columns with the latest values
+      for (int r = 0; r < R; ++r) {
+        const double dg = S[r * R + r];
+        if (dg <= 0.0) continue;
+        double p = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int cc = lane + 32 * q;
+          if (cc < R) p = fma(h[q], S[cc * R + r], p);
+        }
+        const double dot = warp_sum(p);
+        if ((r & 31) == lane) {
+          const int q = r >> 5;
+          const double col = (q ? h[1] : h[0]) + ((q ? m[1] : m[0]) - dot) / dg;
+          const double v = (col < 0.0) ? 0.0 : col;
+          if (q) h[1] = v; else h[0] = v;
+        }
+      }
+    }
+    double* hr = hhat + i * R;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = lane + 32 * q;
+      if (r < R) {
+        hr[r] = h[q];
+        sq[q] = fma(h[q], h[q], sq[q]);
+        bsum = fma(m[q], h[q], bsum);
+      }
+    }
+  }
+  colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket);
+}
+
+// ------------------------------------------------------------------ BPP ----
+// One warp per row: block principal pivoting (updaters.py:121-155) with the
+// passive-set solve done by warp-parallel LU with partial pivoting (dgesv).
+constexpr int kBppWarps = 4;
+
+template <int RP>
+__global__ void __launch_bounds__(kBppWarps * 32)
+    bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
+               int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
+               int* status, unsigned int* ticket) {
+  extern __shared__ __align__(16) double dsm[];
+  constexpr int LP = RP + 1;  // LU pitch (augmented column at index p)
+  double* S = dsm;                                    // R*R
+  double* red = S + RP * RP;                          // kBppWarps * 64
+  double* colbuf = red + kBppWarps * 64;              // RP + 1
+  double* lu = colbuf + RP + 1;                       // kBppWarps * RP * LP
+  load_hadamard(S, grams, order, mode, R);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = lu + size_t(warp) * RP * LP;
+  constexpr int NH = (RP + 31) / 32;  // entries per lane
+  double xs[NH], ys[NH], fs[NH];
+  double sq2[NH];
+#pragma unroll
+  for (int q = 0; q < NH; ++q) sq2[q] = 0.0;
+  double bsum = 0.0;
+
+  for (int64_t i = int64_t(blockIdx.x) * kBppWarps + warp; i < rows; i += int64_t(gridDim.x) * kBppWarps) {
+    const double* fr = mrows + i * R;
+#pragma unroll
+    for (int q = 0; q < NH; ++q) {
+      const int r = lane + 32 * q;
+      fs[q] = (r < R) ? fr[r] : 0.0;
+      xs[q] = 0.0;
+      ys[q] = -fs[q];
+    }
+    unsigned long long P = 0ull;
+    int best = R + 1, backup = 3;
+    bool done = false;
+    int fail_kind = 0;
+    for (int it = 0; it < 5 * R + 1; ++it) {
+      unsigned long long viol = 0ull;
+#pragma unroll
+      for (int q = 0; q < NH; ++q) {
+        const int r = lane + 32 * q;
+        const bool pr = (P >> r) & 1ull;
+        const bool v = (r < R) && ((pr && xs[q] < 0.0) || (!pr && ys[q] < 0.0));
+        viol |= (unsigned long long)__ballot_sync(0xffffffffu, v) << (32 * q);
+      }
+      const int k = __popcll(viol);
+      if (k == 0) {
+        done = true;
+        break;
+      }
+      if (k < best) {
+        best = k;
+        backup = 3;
+        P ^= viol;
+      } else if (backup > 0) {
+        --backup;
+        P ^= viol;
+      } else {
+        P ^= 1ull << (63 - __clzll(viol));
+      }
+      // ---- solve S[P,P] x = f[P] (LU, partial pivoting), y = S[~P,P] x - f[~P]
+      const int p = __popcll(P);
+      // compact passive indices: idx[a] for a < p, built identically by every lane
+      // gather A (p x p) and rhs into this warp's scratch
+      for (int a = lane; a < p; a += 32) {
+        // a-th set bit of P
+        unsigned long long mm = P;
+        for (int t = 0; t < a; ++t) mm &= mm - 1;
+        const int ra = __ffsll(mm) - 1;
+        unsigned long long nn = P;
+        for (int b = 0; b < p; ++b) {
+          const int rb = __ffsll(nn) - 1;
+          nn &= nn - 1;
+          A[a * LP + b] = S[ra * R + rb];
+        }
+        A[a * LP + p] = fr[ra];
+      }
+      __syncwarp();
+      bool singular = false;
+      for (int cidx = 0; cidx < p; ++cidx) {
+        // pivot: max |A[i][c]| over i >= c, first index on ties (idamax)
+        double bv = -1.0;
+        int bi = INT_MAX;
+        for (int a = cidx + lane; a < p; a += 32) {
+          const double v = fabs(A[a * LP + cidx]);
+          if (v > bv) {
+            bv = v;
+            bi = a;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        if (!(bv > 0.0)) {
+          singular = true;
+          break;
+        }
+        if (bi != cidx) {
+          for (int b = lane; b <= p; b += 32) {
+            const double t0 = A[cidx * LP + b];
+            A[cidx * LP + b] = A[bi * LP + b];
+            A[bi * LP + b] = t0;
+          }
+        }
+        __syncwarp();
+        const double inv = 1.0 / A[cidx * LP + cidx];
+        for (int a = cidx + 1 + lane; a < p; a += 32) {
+          const double l = A[a * LP + cidx] * inv;
+          A[a * LP + cidx] = l;
+          for (int b = cidx + 1; b <= p; ++b) A[a * LP + b] = fma(-l, A[cidx * LP + b], A[a * LP + b]);
+        }
+        __syncwarp();
+      }
+      if (singular) {
+        fail_kind = 2;
+        break;
+      }
+      // back substitution, solution overwrites column p
+      for (int a = p - 1; a >= 0; --a) {
+        double s = 0.0;
+        for (int b = a + 1 + lane; b < p; b += 32) s = fma(A[a * LP + b], A[b * LP + p], s);
+        s = warp_sum(s);
+        if (lane == 0) A[a * LP + p] = (A[a * LP + p] - s) / A[a * LP + a];
+        __syncwarp();
+      }
+      // scatter x, compute y on the active set
+#pragma unroll
+      for (int q = 0; q < NH; ++q) {
+        const int r = lane + 32 * q;
+        xs[q] = 0.0;
+        ys[q] = 0.0;
+        if (r < R) {
+          if ((P >> r) & 1ull) {
+            const int a = __popcll(P & ((1ull << r) - 1ull));
+            xs[q] = A[a * LP + p];
+          } else {
+            double s = 0.0;
+            unsigned long long nn = P;
+            for (int b = 0; b < p; ++b) {
+              const int rb = __ffsll(nn) - 1;
+              nn &= nn - 1;
+              s = fma(S[r * R + rb], A[b * LP + p], s);
+            }
+            ys[q] = s - fs[q];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!done && fail_kind == 0) fail_kind = 1;
+    if (fail_kind) {
+      if (lane == 0) {
+        atomicMin(status + 2, int(i));
+        atomicMax(status + 3, fail_kind);
+      }
+    }
+    double* hr = hhat + i * R;
+#pragma unroll
+    for (int q = 0; q < NH; ++q) {
+      const int r = lane + 32 * q;
+      if (r < R) {
+        hr[r] = xs[q];
+        if (beta) bsum = fma(fs[q], xs[q], bsum);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NH; ++q) sq2[q] = fma(xs[q], xs[q], sq2[q]);
+  }
+  __syncthreads();
+  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket);
+}
+
+// --------------------------------------------------- normalise + Gram ------
+constexpr int kGramRows = 64;
+
+template <int RP>
+__global__ void __launch_bounds__(256)
+    normalize_gram_kernel(const double* __restrict__ hhat, const double* __restrict__ nsq, int64_t rows, int R,
+                          double* __restrict__ owned, double* __restrict__ lam, double* __restrict__ gram,
+                          double* __restrict__ part, unsigned int* ticket) {
+  __shared__ double tile[kGramRows * RP];
+  __shared__ double scale[RP];
+  if (threadIdx.x < R) {
+    double s = 1.0;
+    if (nsq) {
+      const double w = sqrt(nsq[threadIdx.x]);
+      s = (w > 0.0) ? w : 1.0;
+      if (blockIdx.x == 0 && lam) lam[threadIdx.x] = w;
+    }
+    scale[threadIdx.x] = s;
+  }
+  __syncthreads();
+  const int64_t r0 = int64_t(blockIdx.x) * kGramRows;
+  const int nr = int(rows - r0 < kGramRows ? rows - r0 : int64_t(kGramRows));
+  for (int e = threadIdx.x; e < nr * R; e += blockDim.x) {
+    const int il = e / R, r = e - (e / R) * R;
+    const int64_t gi = (r0 + il) * R + r;
+    double v = hhat[gi];
+    if (nsq) {
+      v = v / scale[r];
+      owned[gi] = v;
+    }
+    tile[il * RP + r] = v;
+  }
+  __syncthreads();
+  const int RR = R * R;
+  double* mypart = part + size_t(blockIdx.x) * RR;
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    double s = 0.0;
+    for (int il = 0; il < nr; ++il) s = fma(tile[il * RP + a], tile[il * RP + b], s);
+    mypart[e] = s;
+  }
+  if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, RR, gram);
+}
+
+// ------------------------------------------------------------- scalars -----
+__global__ void gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
+                             double* __restrict__ gamma) {
+  __shared__ double v[kMaxRank];
+  const int a = threadIdx.x;
+  if (a < R) {
+    double s = 0.0;
+    for (int b = 0; b < R; ++b) {
+      double p = 1.0;
+      for (int m = 0; m < order; ++m) {
+        const double* g = grams + size_t(m) * R * R;
+        const double sym = 0.5 * (g[a * R + b] + g[b * R + a]);
+        p = (m == 0) ? sym : p * sym;
+      }
+      s = fma(p, lam[b], s);
+    }
+    v[a] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(lam[k], v[k], s);
+    gamma[0] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    inner_kernel(const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ lam,
+                 int64_t rows, int R, double* __restrict__ part, double* out, unsigned int* ticket) {
+  __shared__ double red[8];
+  const int64_t n = rows * R;
+  double s = 0.0;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    double bv = b[e];
+    if (lam) bv = bv * lam[e % R];
+    s = fma(a[e], bv, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (last_cta_ticket(ticket)) {
+    if (threadIdx.x == 0) {
+      double t = part[0];
+      for (unsigned k = 1; k < gridDim.x; ++k) t += part[k];
+      out[0] = t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512)
+    norm_sq_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part, double* out,
+                   unsigned int* ticket) {
+  __shared__ double red[16];
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t n2 = n / 2;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n2; e += int64_t(gridDim.x) * blockDim.x) {
+    const double2 v = __ldcs(x2 + e);
+    s0 = fma(v.x, v.x, s0);
+    s1 = fma(v.y, v.y, s1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s0 = fma(x[n - 1], x[n - 1], s0);
+  const double s = block_sum(s0 + s1, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (last_cta_ticket(ticket)) {
+    if (threadIdx.x == 0) {
+      double t = part[0];
+      for (unsigned k = 1; k < gridDim.x; ++k) t += part[k];
+      out[0] = t;
+    }
+  }
+}
+
+__global__ void status_reset_kernel(int* status) {
+  status[0] = 0;
+  status[1] = 0;
+  status[2] = INT_MAX;
+  status[3] = 0;
+}
+
+// ------------------------------------------------------------- host side ---
+#define NNCP_RP_CASES(RPV, ...)            \
+  switch (RPV) {                            \
+    case 8: { constexpr int RP = 8; __VA_ARGS__; } break;   \
+    case 16: { constexpr int RP = 16; __VA_ARGS__; } break; \
+    case 24: { constexpr int RP = 24; __VA_ARGS__; } break; \
+    case 32: { constexpr int RP = 32; __VA_ARGS__; } break; \
+    case 40: { constexpr int RP = 40; __VA_ARGS__; } break; \
+    case 48: { constexpr int RP = 48; __VA_ARGS__; } break; \
+    case 56: { constexpr int RP = 56; __VA_ARGS__; } break; \
+    case 64: { constexpr int RP = 64; __VA_ARGS__; } break; \
+    default: return fail(NNCP_ERR_UNSUPPORTED, "rank above NNCP_MAX_RANK"); \
+  }
+
+int row_blocks(int64_t rows) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + kRowWarps - 1) / kRowWarps, int64_t(num_sms()) * 4)));
+}
+
+size_t row_update_part_elems(int64_t rows, int rank) {
+  const int64_t blocks_rows = row_blocks(rows);
+  const int64_t blocks_bpp = std::min<int64_t>((rows + kBppWarps - 1) / kBppWarps, int64_t(num_sms()) * 4);
+  const int64_t blocks_gram = (rows + kGramRows - 1) / kGramRows;
+  size_t e = std::max<int64_t>(blocks_rows, blocks_bpp) * (rank + 1);
+  e = std::max<size_t>(e, size_t(std::max<int64_t>(blocks_gram, 1)) * rank * rank);
+  e = std::max<size_t>(e, size_t(num_sms()) * 8);
+  return e;
+}
+
+int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
+           const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
+           size_t ws_bytes, cudaStream_t st) {
+  if (rows <= 0) {
+    // an empty row block still owes its (zero) column sums
+    if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
+    if (beta) NNCP_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), st));
+    return NNCP_OK;
+  }
+  WsLayout w = ws_layout(ws, ws_bytes);
+  const int rp = pad8(rank);
+  (void)rp;
+  if (algo == NNCP_ALGO_MU || algo == NNCP_ALGO_HALS) {
+    const int blocks = row_blocks(rows);
+    if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (update)");
+    if (algo == NNCP_ALGO_MU)
+      update_rows_kernel<NNCP_ALGO_MU><<<blocks, kRowWarps * 32, 0, st>>>(
+          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE);
+    else
+      update_rows_kernel<NNCP_ALGO_HALS><<<blocks, kRowWarps * 32, 0, st>>>(
+          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE);
+  } else if (algo == NNCP_ALGO_BPP) {
+    const int blocks = int(std::min<int64_t>((rows + kBppWarps - 1) / kBppWarps, int64_t(num_sms()) * 4));
+    if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
+    NNCP_RP_CASES(rp, {
+      const size_t smem = sizeof(double) * (size_t(RP) * RP + kBppWarps * 64 + RP + 1 +
+                                            size_t(kBppWarps) * RP * (RP + 1));
+      static bool attr = false;
+      if (!attr) {
+        NNCP_CUDA_TRY(cudaFuncSetAttribute(bpp_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+      }
+      bpp_kernel<RP><<<blocks, kBppWarps * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
+                                                           beta, status, w.tickets + T_UPDATE);
+    });
+  } else {
+    return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");
+  }
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
+                   double* gram, void* ws, size_t ws_bytes, cudaStream_t st, int ticket_slot) {
+  WsLayout w = ws_layout(ws, ws_bytes);
+  const int rp = pad8(rank);
+  const int blocks = int(std::max<int64_t>(1, (rows + kGramRows - 1) / kGramRows));
+  if (w.part_elems < size_t(blocks) * rank * rank) return fail(NNCP_ERR_VALUE, "workspace too small (gram)");
+  NNCP_RP_CASES(rp, (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
+                                                                      owned, lam, gram, w.part,
+                                                                      w.tickets + ticket_slot)));
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int gamma(const double* grams, int order, int rank, const double* lam, double* out, cudaStream_t st) {
+  gamma_kernel<<<1, 64, 0, st>>>(grams, order, rank, lam, out);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int inner(const double* a, const double* b, const double* lam, int64_t rows, int rank, double* out, void* ws,
+          size_t ws_bytes, cudaStream_t st) {
+  WsLayout w = ws_layout(ws, ws_bytes);
+  const int64_t n = rows * rank;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 4)));
+  if (w.part_elems < size_t(blocks)) return fail(NNCP_ERR_VALUE, "workspace too small (inner)");
+  inner_kernel<<<blocks, 256, 0, st>>>(a, b, lam, rows, rank, w.part, out, w.tickets + T_INNER);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  WsLayout w = ws_layout(ws, ws_bytes);
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n / 2 + 511) / 512, int64_t(num_sms()) * 8)));
+  if (w.part_elems < size_t(blocks)) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
+  if (reinterpret_cast<uintptr_t>(x) % 16) return fail(NNCP_ERR_VALUE, "tensor must be 16-byte aligned");
+  norm_sq_kernel<<<blocks, 512, 0, st>>>(x, n, w.part, out, w.tickets + T_NORM);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int status_reset(int* status, cudaStream_t st) {
+  status_reset_kernel<<<1, 1, 0, st>>>(status);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+}  // namespace nncp

@@ -1,0 +1,556 @@
+"""NNCP alternating-update driver on B200 (reference: nncp/driver.py).
+
+Public surface identical to the reference (driver.py:46-56, 73-134, 495-531):
+``RunConfig``, ``RunReport``, ``record_category``, ``init_factor``,
+``relative_error``, ``nncp_sequential``, ``nncp_parallel``, ``CATEGORIES``,
+``ALGORITHMS``.  The inner program is the reference's ``_run_spmd``
+(driver.py:331-449) with every numeric step on the GPU:
+
+    per mode n:  MTTKRP (dimension tree: DMMA partial GEMMs + TTV kernels)
+                 -> Reduce-Scatter(slice)            [identity on one GPU]
+                 -> fused Hadamard + MU/HALS/BPP update + column sums (+ beta)
+                 -> All-Reduce(nsq) -> fused normalise + Gram -> All-Reduce(Gram)
+                 -> All-Gather(slice)
+    per sweep:   All-Reduce(beta), gamma kernel, one 2-scalar + status D2H
+
+Host work per iteration is kernel launches plus that one small read-back;
+optionally the whole sweep is replayed as a CUDA graph (``cuda_graph=True``).
+Category seconds come from CUDA events on the launching stream.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dimtree import DimTreeContext, DimTreePlan
+from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, RankLayout, ThreadCollectives,
+                   ThreadGrid, block_partition)
+from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
+from .updaters import BppCyclingError, raise_for_status  # noqa: F401  (re-exported semantics)
+
+__all__ = ["ALGORITHMS", "CATEGORIES", "RunConfig", "RunReport", "init_factor", "nncp_parallel",
+           "nncp_sequential", "record_category", "relative_error", "IN_SCOPE_ALGORITHMS", "run_local"]
+
+CATEGORIES = ("MTTKRP", "KRP", "MultiTTV", "Gram", "NNLS", "ReduceScatter", "AllGather", "AllReduce", "Error")
+ALGORITHMS = ("ucp", "mu", "hals", "bpp", "admm", "nes")
+IN_SCOPE_ALGORITHMS = ("mu", "hals", "bpp")
+
+
+@dataclass
+class RunConfig:
+    """Knobs of one decomposition run (driver.py:73-101); ``cuda_graph`` is device-only."""
+
+    rank: int
+    algorithm: str = "bpp"
+    max_iters: int = 100
+    tol: float = 1e-6
+    seed: int = 0
+    grid: tuple = None
+    use_dimtree: bool = True
+    strict_split: bool = False
+    initial_factors: FactorSet = None
+    cuda_graph: bool = False
+
+    def validate(self, order: int):
+        if self.rank < 1:
+            raise ValueError("rank must be at least 1")
+        if self.tol < 0:
+            raise ValueError("tolerance must be nonnegative")
+        if self.max_iters < 0:
+            raise ValueError("max_iters must be nonnegative")
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"unknown algorithm {self.algorithm!r}")
+        if self.grid is not None and len(self.grid) != order:
+            raise ValueError(f"grid order {len(self.grid)} does not match tensor order {order}")
+        if self.initial_factors is not None and self.initial_factors.rank != self.rank:
+            raise ValueError("initial factors disagree with configured rank")
+        if self.algorithm not in IN_SCOPE_ALGORITHMS:
+            raise NotImplementedError(
+                f"algorithm {self.algorithm!r} is outside this build's hot-path scope "
+                f"(supported: {', '.join(IN_SCOPE_ALGORITHMS)})")
+        if self.rank > _lib.MAX_RANK:
+            raise NotImplementedError(f"rank {self.rank} exceeds the device limit {_lib.MAX_RANK}")
+        if order > _lib.MAX_ORDER:
+            raise NotImplementedError(f"tensor order {order} exceeds the device limit {_lib.MAX_ORDER}")
+
+
+@dataclass
+class RunReport:
+    """Error curve plus timing / communication breakdown (driver.py:104-126)."""
+
+    errors: list = field(default_factory=list)
+    rows: list = field(default_factory=list)
+    row_words: list = field(default_factory=list)
+    row_wall: list = field(default_factory=list)
+    counters: CommCounters = field(default_factory=CommCounters)
+    model: FactorSet = None
+    converged: bool = False
+    split_mode: int = None
+    tree_partial_calls: int = 0
+
+    def begin_row(self):
+        self.rows.append({c: 0.0 for c in CATEGORIES})
+        self.row_words.append(0)
+        self.row_wall.append(0.0)
+
+
+def record_category(report: RunReport, category: str, elapsed: float, words: int = 0):
+    """driver.py:129-134."""
+    if category not in CATEGORIES:
+        raise ValueError(f"unknown category {category!r}")
+    report.rows[-1][category] += elapsed
+    report.row_words[-1] += words
+
+
+def init_factor(seed: int, mode: int, rows: int, rank: int) -> np.ndarray:
+    """Uniform [0,1) factor, Philox keyed by (seed, mode) (driver.py:137-143).
+
+    Generated on the host with numpy's Philox so the draws are bit-identical
+    to the reference; uploaded once per run.
+    """
+    key = np.array([np.uint64(seed), np.uint64(mode)], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key)).random((rows, rank))
+
+
+def _eps_from_terms(alpha: float, beta: float, gamma: float) -> float:
+    """driver.py:146-148 (host arithmetic on three device-reduced scalars)."""
+    return float(np.sqrt(max(0.0, alpha - 2.0 * beta + gamma) / alpha))
+
+
+def relative_error(alpha, mttkrp_n, h_n_unnormalized, s_n, g_n, lam) -> float:
+    """driver.py:151-162 with beta / gamma reduced on the device."""
+    if alpha <= 0.0:
+        raise ValueError("zero tensor has no relative error")
+    lib = _lib.load()
+    m = as_device(mttkrp_n)
+    h = as_device(h_n_unnormalized)
+    if tuple(m.shape) != tuple(h.shape):
+        raise ValueError(f"shape mismatch: {tuple(m.shape)} vs {tuple(h.shape)}")
+    r = int(m.shape[1])
+    lam_d = as_device(lam)
+    pair = torch.stack([as_device(s_n), as_device(g_n)]).contiguous()
+    out = torch.empty(2, dtype=torch.float64, device=m.device)
+    ws = Workspace(1 << 20)
+    st = _lib.stream_handle()
+    _lib.check(lib.nncp_inner(_lib.ptr(m), _lib.ptr(h), None, int(m.shape[0]), r, _lib.ptr(out), ws.ptr, ws.nbytes,
+                              st))
+    _lib.check(lib.nncp_gamma(_lib.ptr(pair), 2, r, _lib.ptr(lam_d), _lib.vp(out.data_ptr() + 8), st))
+    beta, gamma = out.cpu().tolist()
+    return _eps_from_terms(float(alpha), beta, gamma)
+
+
+# ------------------------------------------------------------ timing --------
+
+class _EventTimer:
+    """Category seconds from CUDA events recorded at phase boundaries."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self._pool = []
+        self._marks = []
+        self._start = None
+
+    def _event(self):
+        if self._pool:
+            return self._pool.pop()
+        return torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        if not self.enabled:
+            return
+        self._start = self._event()
+        self._start.record()
+        self._marks = []
+
+    def mark(self, category):
+        if not self.enabled:
+            return
+        e = self._event()
+        e.record()
+        self._marks.append((category, e))
+
+    def collect(self, row: dict):
+        """Accumulate (after the stream is synchronised) into ``row``."""
+        if not self.enabled or self._start is None:
+            return
+        prev = self._start
+        for cat, e in self._marks:
+            row[cat] += prev.elapsed_time(e) / 1e3
+            self._pool.append(prev)
+            prev = e
+        self._pool.append(prev)
+        self._marks = []
+        self._start = None
+
+
+# ------------------------------------------------------------ engine --------
+
+class _Engine:
+    """One execution context (one GPU, or one simulated worker) of the SPMD program."""
+
+    def __init__(self, x_local: torch.Tensor, local_dims, global_dims, cfg: RunConfig, coll, layout=None,
+                 timing: bool = True):
+        self.x = x_local
+        self.dims = tuple(int(d) for d in local_dims)
+        self.global_dims = tuple(int(d) for d in global_dims)
+        self.cfg = cfg
+        self.coll = coll
+        self.layout = layout
+        self.N = len(self.dims)
+        self.R = int(cfg.rank)
+        self.algo = _lib.ALGO_CODES[cfg.algorithm]
+        dev = x_local.device
+        self.dev = dev
+        if layout is None:
+            self.owned_rows = [slice(0, d) for d in self.global_dims]
+            self.slice_rows = [slice(0, d) for d in self.global_dims]
+            self.owned_parts = [block_partition(d, 1) for d in self.dims]
+        else:
+            self.owned_rows = list(layout.owned_rows)
+            self.slice_rows = list(layout.slice_rows)
+            self.owned_parts = list(layout.owned_parts)
+        self.n_owned = [s.stop - s.start for s in self.owned_rows]
+        self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
+        self.ws = Workspace(self.plan.workspace_bytes())
+        self.ctx = DimTreeContext(self.plan, workspace=self.ws)
+        f64 = dict(dtype=torch.float64, device=dev)
+        R, N = self.R, self.N
+        self.grams = torch.zeros((N, R, R), **f64)
+        self.lam = torch.ones(R, **f64)
+        self.nsq = torch.zeros(R, **f64)
+        self.scal = torch.zeros(4, **f64)           # beta, gamma, alpha, beta0
+        self.status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32, device=dev)
+        self.mbar = torch.empty((max(self.dims), R), **f64)
+        self.hhat = torch.empty((max(max(self.n_owned), 1), R), **f64)
+        self.owned = [torch.empty((self.n_owned[n], R), **f64) for n in range(N)]
+        if coll.parallel:
+            self.shared = [torch.empty((self.dims[n], R), **f64) for n in range(N)]
+        else:
+            self.shared = self.owned
+        self.host_scal = torch.zeros(2, dtype=torch.float64).pin_memory()
+        self.host_status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32).pin_memory()
+        self.timer = _EventTimer(timing)
+        self.lib = _lib.load()
+        self.graph = None
+        self.report = RunReport()
+
+    # -- small wrappers -------------------------------------------------------
+    def _st(self):
+        return _lib.stream_handle()
+
+    def _gather(self, n):
+        if self.coll.parallel:
+            out = self.coll.all_gather(n, self.owned[n], self.owned_parts[n])
+            self.shared[n].copy_(out)
+
+    # -- initialisation (driver.py:338-373) -----------------------------------
+    def initialise(self):
+        lib, st, R = self.lib, self._st(), self.R
+        self.report.begin_row()
+        wall0 = time.perf_counter()
+        self.timer.start()
+        _lib.check(lib.nncp_norm_squared(_lib.ptr(self.x), self.x.numel(), _lib.vp(self.scal.data_ptr() + 16),
+                                         self.ws.ptr, self.ws.nbytes, st))
+        self.timer.mark("Error")
+        alpha_t = self.scal[2:3]
+        self.coll.all_reduce(alpha_t)
+        self.timer.mark("AllReduce")
+        self.alpha = float(alpha_t.item())
+        if self.alpha <= 0.0:
+            raise ValueError("zero tensor has no relative error")
+        cfg = self.cfg
+        for n, size in enumerate(self.global_dims):
+            if cfg.initial_factors is not None:
+                full = cfg.initial_factors.factors[n]
+                full = full.detach().cpu().numpy() if isinstance(full, torch.Tensor) else np.asarray(full, np.float64)
+                if full.shape != (size, R):
+                    raise ValueError(f"initial factor {n} has shape {full.shape}")
+            else:
+                full = init_factor(cfg.seed, n, size, R)
+            self.owned[n].copy_(torch.from_numpy(np.ascontiguousarray(full[self.owned_rows[n]])))
+            if self.coll.parallel:
+                self.shared[n].copy_(torch.from_numpy(np.ascontiguousarray(full[self.slice_rows[n]])))
+        if cfg.initial_factors is not None:
+            lam0 = cfg.initial_factors.lam
+            lam0 = lam0.detach().cpu().numpy() if isinstance(lam0, torch.Tensor) else np.asarray(lam0, np.float64)
+            self.lam.copy_(torch.from_numpy(np.ascontiguousarray(lam0)))
+        self.timer.mark("Error")
+        for n in range(self.N):
+            _lib.check(lib.nncp_gram(_lib.ptr(self.owned[n]), self.n_owned[n], R, _lib.ptr(self.grams[n]),
+                                     self.ws.ptr, self.ws.nbytes, st))
+            self.timer.mark("Gram")
+            self.coll.all_reduce(self.grams[n])
+            self.timer.mark("AllReduce")
+            self._gather(n)
+            self.timer.mark("AllGather")
+        self.report.split_mode = self.plan.split if cfg.use_dimtree else None
+        # initial model error from an out-of-band last-mode MTTKRP (driver.py:362-373);
+        # the reference uses the einsum oracle here, the device reuses the tree kernels
+        calls = self.ctx.partial_calls
+        mb = self.mbar[: self.dims[-1]]
+        self.ctx.mttkrp_last_mode(self.x, self.shared, out=mb)
+        self.ctx.partial_calls = calls
+        self.timer.mark("MTTKRP")
+        _lib.check(lib.nncp_inner(_lib.ptr(mb), _lib.ptr(self.shared[-1]), _lib.ptr(self.lam), self.dims[-1], R,
+                                  _lib.vp(self.scal.data_ptr() + 24), self.ws.ptr, self.ws.nbytes, st))
+        self.timer.mark("Error")
+        self.coll.all_reduce(self.scal[3:4])
+        self.timer.mark("AllReduce")
+        _lib.check(lib.nncp_gamma(_lib.ptr(self.grams), self.N, R, _lib.ptr(self.lam),
+                                  _lib.vp(self.scal.data_ptr() + 8), st))
+        self.timer.mark("Error")
+        beta0, gamma0 = self.scal[3].item(), self.scal[1].item()
+        self.report.errors = [_eps_from_terms(self.alpha, beta0, gamma0)]
+        self.timer.collect(self.report.rows[-1])
+        self.report.row_wall[-1] = time.perf_counter() - wall0
+        self.report.row_words[-1] = self.coll.counters.total_words()
+
+    # -- one outer iteration (driver.py:380-433), launches only ----------------
+    def _sweep(self):
+        lib, st, R, N = self.lib, self._st(), self.R, self.N
+        cfg = self.cfg
+        if cfg.use_dimtree:
+            self.ctx.begin_iteration()
+        for n in range(N):
+            _lib.check(lib.nncp_status_reset(_lib.ptr(self.status[n]), st))
+            mb = self.mbar[: self.dims[n]]
+            if cfg.use_dimtree:
+                self.ctx.mttkrp(self.x, self.shared, n, out=mb)
+            else:
+                self.ctx.mttkrp_direct(self.x, self.shared, n, out=mb)
+            self.timer.mark("MTTKRP")
+            m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
+            self.timer.mark("ReduceScatter")
+            last = n == N - 1
+            _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
+                                       _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
+                                       _lib.ptr(self.hhat), _lib.ptr(self.nsq),
+                                       _lib.ptr(self.scal) if last else None, _lib.ptr(self.status[n]),
+                                       self.ws.ptr, self.ws.nbytes, st))
+            self.timer.mark("NNLS")
+            self.coll.all_reduce(self.nsq)
+            self.timer.mark("AllReduce")
+            _lib.check(lib.nncp_normalize_gram(_lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R,
+                                               _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
+                                               _lib.ptr(self.grams[n]), self.ws.ptr, self.ws.nbytes, st))
+            self.timer.mark("Gram")
+            self.coll.all_reduce(self.grams[n])
+            self.timer.mark("AllReduce")
+            self._gather(n)
+            self.timer.mark("AllGather")
+        self.coll.all_reduce(self.scal[0:1])
+        self.timer.mark("AllReduce")
+        _lib.check(lib.nncp_gamma(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam), _lib.vp(self.scal.data_ptr() + 8),
+                                  st))
+        self.host_scal.copy_(self.scal[0:2], non_blocking=True)
+        self.host_status.copy_(self.status, non_blocking=True)
+        self.timer.mark("Error")
+
+    def _finish_iteration(self, it):
+        torch.cuda.current_stream().synchronize()
+        status = self.host_status.tolist()
+        for n in range(self.N):
+            try:
+                raise_for_status(status[n], warn_hals=(self.cfg.algorithm == "hals"))
+            except Exception as exc:
+                raise RuntimeError(f"NNLS update failed at iteration {it}, mode {n + 1}") from exc
+        beta, gamma = self.host_scal.tolist()
+        return _eps_from_terms(self.alpha, beta, gamma)
+
+    def iterate(self):
+        cfg = self.cfg
+        errors = self.report.errors
+        use_graph = cfg.cuda_graph and not self.coll.parallel
+        converged = False
+        for it in range(1, cfg.max_iters + 1):
+            self.report.begin_row()
+            wall0 = time.perf_counter()
+            if use_graph and self.graph is None and it > 1:
+                self._capture()
+            if self.graph is not None:
+                self.graph.replay()
+                if cfg.use_dimtree:
+                    self.ctx.partial_calls += 2
+            else:
+                self.timer.start()
+                self._sweep()
+            eps = self._finish_iteration(it)
+            self.timer.collect(self.report.rows[-1])
+            errors.append(eps)
+            self.report.row_wall[-1] = time.perf_counter() - wall0
+            self.report.row_words[-1] = self.coll.counters.total_words() - sum(self.report.row_words[:-1])
+            if eps <= cfg.tol:
+                converged = True
+                break
+        self.report.converged = converged
+        self.report.tree_partial_calls = self.ctx.partial_calls if cfg.use_dimtree else 0
+
+    def _capture(self):
+        """Record one sweep as a CUDA graph (all buffers already allocated by sweep 1)."""
+        timing = self.timer.enabled
+        self.timer.enabled = False
+        calls = self.ctx.partial_calls
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self._sweep()
+        torch.cuda.current_stream().wait_stream(side)
+        self.ctx.partial_calls = calls
+        self.graph = g
+        self.timer.enabled = timing
+
+    def model_host(self):
+        return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()
+
+
+def _warn_if_negative(x: DenseTensor, cfg: RunConfig):
+    """driver.py:571-573 (min over the device copy)."""
+    if cfg.algorithm == "ucp":
+        return
+    d = x.data
+    lo = float(torch.min(d).item()) if isinstance(d, torch.Tensor) else float(np.min(d))
+    if lo < 0.0:
+        warnings.warn("tensor has negative entries; nonnegative model will not fit")
+
+
+def run_local(x_local: torch.Tensor, local_dims, global_dims, cfg: RunConfig, coll=None, layout=None,
+              timing: bool = True):
+    """Run the SPMD program on one execution context; returns (engine, report)."""
+    eng = _Engine(x_local, local_dims, global_dims, cfg, coll or IdentityCollectives(), layout, timing)
+    eng.initialise()
+    eng.iterate()
+    eng.report.counters = eng.coll.counters
+    return eng, eng.report
+
+
+def nncp_sequential(x: DenseTensor, cfg: RunConfig) -> RunReport:
+    """Single-GPU NNCP (driver.py:495-505); the tensor is copied to HBM once if needed."""
+    cfg.validate(x.order)
+    if cfg.grid is not None and int(np.prod(cfg.grid)) != 1:
+        raise ValueError("sequential driver got a nontrivial grid; use nncp_parallel")
+    xd = x.to_device()
+    _warn_if_negative(xd, cfg)
+    eng, rep = run_local(xd.data, x.dims, x.dims, cfg)
+    owned, lam = eng.model_host()
+    rep.model = FactorSet(owned, lam)
+    return rep
+
+
+def nncp_parallel(x: DenseTensor, cfg: RunConfig) -> RunReport:
+    """Grid-parallel NNCP (driver.py:508-531).
+
+    Inside a torch.distributed job whose world size equals prod(grid), each
+    process runs its grid block on its own GPU (NCCL collectives) and every
+    rank returns the merged report.  Otherwise the grid is simulated by worker
+    threads on the local GPU with rank-ordered, bitwise-reproducible
+    collectives (the reference's execution model, grid.py:172-203).
+    """
+    cfg.validate(x.order)
+    if cfg.grid is None:
+        raise ValueError("parallel driver needs a grid shape")
+    for n, (i, p) in enumerate(zip(x.dims, cfg.grid)):
+        if p > i:
+            raise ValueError(f"grid dim {p} exceeds tensor dim {i} in mode {n + 1}; "
+                             "every worker must hold a nonempty tensor block")
+    grid = Grid(cfg.grid)
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() == grid.total:
+        return _parallel_dist(x, cfg, grid)
+    return _parallel_threads(x, cfg, grid)
+
+
+def _local_block(x: DenseTensor, layout: RankLayout) -> torch.Tensor:
+    arr = x.as_array()[tuple(layout.slice_rows)]
+    return as_device(np.asarray(arr).ravel(order="F"))
+
+
+def _parallel_threads(x: DenseTensor, cfg: RunConfig, grid: Grid) -> RunReport:
+    tgrid = ThreadGrid(grid)
+    results = [None] * grid.total
+    failures = [None] * grid.total
+    dev = torch.cuda.current_device()
+    hostx = DenseTensor(x.dims, x.host_data())
+    _warn_if_negative(hostx, cfg)
+
+    def main(rank):
+        try:
+            torch.cuda.set_device(dev)
+            layout = RankLayout(grid, rank, x.dims)
+            xl = _local_block(hostx, layout)
+            coll = ThreadCollectives(tgrid, layout)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                eng, rep = run_local(xl, layout.local_dims, x.dims, cfg, coll, layout)
+                owned, lam = eng.model_host()
+            results[rank] = (rep, owned, lam, layout.owned_rows)
+        except threading.BrokenBarrierError:
+            pass
+        except BaseException as exc:  # noqa: BLE001  (propagate to the caller)
+            failures[rank] = exc
+            tgrid.abort()
+
+    threads = [threading.Thread(target=main, args=(r,), name=f"nncp-worker-{r}") for r in range(grid.total)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for exc in failures:
+        if exc is not None:
+            raise exc
+    return _merge_reports(results, x.dims, cfg.rank)
+
+
+def _parallel_dist(x: DenseTensor, cfg: RunConfig, grid: Grid) -> RunReport:
+    import torch.distributed as dist
+
+    rank = dist.get_rank()
+    layout = RankLayout(grid, rank, x.dims)
+    coll = DistCollectives(layout)
+    xl = _local_block(DenseTensor(x.dims, x.host_data()), layout)
+    if rank == 0:
+        _warn_if_negative(x, cfg)
+    eng, rep = run_local(xl, layout.local_dims, x.dims, cfg, coll, layout)
+    owned, lam = eng.model_host()
+    gathered = [None] * grid.total
+    dist.all_gather_object(gathered, (rep, owned, lam, layout.owned_rows))
+    return _merge_reports(gathered, x.dims, cfg.rank)
+
+
+def _merge_reports(results, dims, rank) -> RunReport:
+    """driver.py:534-568: averaged seconds, summed words and counters, assembled model."""
+    merged = RunReport()
+    first = results[0][0]
+    nworkers = len(results)
+    merged.errors = list(first.errors)
+    merged.split_mode = first.split_mode
+    merged.converged = first.converged
+    merged.tree_partial_calls = first.tree_partial_calls
+    for rep, _, _, _ in results:
+        if not np.allclose(rep.errors, first.errors, rtol=0, atol=1e-12):
+            raise AssertionError("workers disagree on the error sequence")
+    for k in range(len(first.rows)):
+        merged.begin_row()
+        for cat in CATEGORIES:
+            merged.rows[k][cat] = sum(r.rows[k][cat] for r, _, _, _ in results) / nworkers
+        merged.row_words[k] = sum(r.row_words[k] for r, _, _, _ in results)
+        merged.row_wall[k] = sum(r.row_wall[k] for r, _, _, _ in results) / nworkers
+    counters = CommCounters()
+    for rep, _, _, _ in results:
+        counters = counters.merged_with(rep.counters)
+    merged.counters = counters
+    factors = [np.zeros((i, rank)) for i in dims]
+    for _, owned, _, rows in results:
+        for n, (h, s) in enumerate(zip(owned, rows)):
+            factors[n][s] = h
+    merged.model = FactorSet(factors, results[0][2])
+    return merged

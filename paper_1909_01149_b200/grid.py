@@ -1,0 +1,374 @@
+"""N-d processor grid and the three collectives of the NNCP step (reference: nncp/grid.py).
+
+Grid semantics are the reference's (grid.py:129-170): rank = p_1 + P_1 p_2 + ...
+(mode-1 coordinate fastest), the mode-n slice of a rank is every rank sharing
+its n-th coordinate (sorted), tensor blocks and owned factor rows come from
+``block_partition`` (first ``length % parts`` blocks get one extra row).
+
+Three interchangeable collective backends sit behind one interface
+(``all_reduce`` / ``reduce_scatter`` / ``all_gather``, the swap point the
+reference documents at pkg/README.md:133-136):
+
+* ``IdentityCollectives`` -- one context, every collective is the identity;
+* ``DistCollectives``     -- one process per GPU over ``torch.distributed``
+  (NCCL over NVLink/NVSwitch on the B200 box; gloo for the CPU tests), one
+  global group plus one sub-group per mode slice;
+* ``ThreadCollectives``   -- workers as threads in one process sharing the
+  local GPU(s); rank-ordered device-side reductions, bitwise reproducible
+  (what ``nncp_parallel`` uses when no process group is running).
+
+Word counters follow CommCounters (grid.py:60-93): words_in = elements
+entering the call, words_out = elements leaving it.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+__all__ = ["block_partition", "DistMap", "CommCounters", "Group", "Grid", "IdentityCollectives",
+           "DistCollectives", "ThreadCollectives", "ThreadGrid"]
+
+
+def block_partition(length: int, parts: int) -> "DistMap":
+    """Balanced contiguous blocks, first length % parts get +1 (grid.py:25-31)."""
+    if length < 0 or parts < 1:
+        raise ValueError(f"bad partition request: length={length}, parts={parts}")
+    base, extra = divmod(int(length), int(parts))
+    return DistMap([base + 1 if k < extra else base for k in range(parts)])
+
+
+class DistMap:
+    """Contiguous block partition of [0, I) (grid.py:34-57)."""
+
+    __slots__ = ("lengths", "offsets")
+
+    def __init__(self, lengths):
+        self.lengths = tuple(int(x) for x in lengths)
+        if any(x < 0 for x in self.lengths):
+            raise ValueError("block lengths must be nonnegative")
+        offs = [0]
+        for x in self.lengths:
+            offs.append(offs[-1] + x)
+        self.offsets = tuple(offs)
+
+    @property
+    def total(self) -> int:
+        return self.offsets[-1]
+
+    @property
+    def parts(self) -> int:
+        return len(self.lengths)
+
+    @property
+    def max_length(self) -> int:
+        return max(self.lengths) if self.lengths else 0
+
+    def block(self, k: int) -> slice:
+        return slice(self.offsets[k], self.offsets[k + 1])
+
+
+@dataclass
+class CommCounters:
+    """Per-rank tallies of collective calls, words and seconds (grid.py:60-93)."""
+
+    calls: dict = field(default_factory=dict)
+    words_in: dict = field(default_factory=dict)
+    words_out: dict = field(default_factory=dict)
+    seconds: dict = field(default_factory=dict)
+
+    def record(self, name: str, words_in: int, words_out: int, elapsed: float = 0.0):
+        self.calls[name] = self.calls.get(name, 0) + 1
+        self.words_in[name] = self.words_in.get(name, 0) + int(words_in)
+        self.words_out[name] = self.words_out.get(name, 0) + int(words_out)
+        self.seconds[name] = self.seconds.get(name, 0.0) + elapsed
+
+    def snapshot(self) -> dict:
+        return {"calls": dict(self.calls), "words_in": dict(self.words_in), "words_out": dict(self.words_out)}
+
+    def total_words(self) -> int:
+        return sum(self.words_in.values()) + sum(self.words_out.values())
+
+    def merged_with(self, other: "CommCounters") -> "CommCounters":
+        out = CommCounters()
+        for src in (self, other):
+            for name, c in src.calls.items():
+                out.calls[name] = out.calls.get(name, 0) + c
+                out.words_in[name] = out.words_in.get(name, 0) + src.words_in.get(name, 0)
+                out.words_out[name] = out.words_out.get(name, 0) + src.words_out.get(name, 0)
+                out.seconds[name] = out.seconds.get(name, 0.0) + src.seconds.get(name, 0.0)
+        return out
+
+
+class Group:
+    """Sorted rank set with position lookup (grid.py:116-126)."""
+
+    def __init__(self, ranks):
+        self.ranks = tuple(sorted(int(r) for r in ranks))
+        self.index = {r: k for k, r in enumerate(self.ranks)}
+
+    @property
+    def size(self) -> int:
+        return len(self.ranks)
+
+
+class Grid:
+    """P_1 x ... x P_N grid; rank <-> coordinate with mode-1 fastest (grid.py:129-170)."""
+
+    def __init__(self, shape):
+        self.shape = tuple(int(p) for p in shape)
+        if any(p < 1 for p in self.shape):
+            raise ValueError(f"grid dims must be positive, got {self.shape}")
+        self.total = int(np.prod(self.shape))
+        self.all_procs = Group(range(self.total))
+        self.slice_groups = []
+        for n, pn in enumerate(self.shape):
+            groups = [[] for _ in range(pn)]
+            for rank in range(self.total):
+                groups[self.coord_of(rank)[n]].append(rank)
+            self.slice_groups.append([Group(g) for g in groups])
+
+    def coord_of(self, rank: int):
+        coord = []
+        for p in self.shape:
+            rank, c = divmod(rank, p)
+            coord.append(c)
+        return tuple(coord)
+
+    def rank_of(self, coord) -> int:
+        rank, stride = 0, 1
+        for c, p in zip(coord, self.shape):
+            if not 0 <= c < p:
+                raise ValueError(f"coordinate {coord} outside grid {self.shape}")
+            rank += c * stride
+            stride *= p
+        return rank
+
+    def slice_group(self, mode: int, coord: int) -> Group:
+        return self.slice_groups[mode][coord]
+
+
+# ------------------------------------------------------------- layout ------
+
+class RankLayout:
+    """Tensor block and owned factor rows of one rank (driver.py:223-246)."""
+
+    def __init__(self, grid: Grid, rank: int, global_dims):
+        self.grid = grid
+        self.rank = rank
+        self.coord = grid.coord_of(rank)
+        self.global_dims = tuple(int(d) for d in global_dims)
+        tensor_maps = [block_partition(i, p) for i, p in zip(self.global_dims, grid.shape)]
+        self.slice_rows = [m.block(c) for m, c in zip(tensor_maps, self.coord)]
+        self.local_dims = tuple(s.stop - s.start for s in self.slice_rows)
+        self.groups = [grid.slice_group(n, c) for n, c in enumerate(self.coord)]
+        self.owned_parts = []
+        self.owned_rows = []
+        for n, s in enumerate(self.slice_rows):
+            parts = block_partition(s.stop - s.start, self.groups[n].size)
+            local = parts.block(self.groups[n].index[rank])
+            self.owned_rows.append(slice(s.start + local.start, s.start + local.stop))
+            self.owned_parts.append(parts)
+
+
+# ------------------------------------------------------------ backends ------
+
+class IdentityCollectives:
+    """Single execution context: collectives are the identity (driver.py:186-215)."""
+
+    parallel = False
+
+    def __init__(self):
+        self.counters = CommCounters()
+
+    def all_reduce(self, t, op="sum"):
+        return t
+
+    def reduce_scatter(self, mode, t, parts=None):
+        return t
+
+    def all_gather(self, mode, t, parts=None):
+        return t
+
+
+class DistCollectives:
+    """torch.distributed backend, one process per GPU (NCCL) or per CPU rank (gloo).
+
+    Ragged row blocks are zero-padded to the slice group's longest block so the
+    equal-count NCCL collectives apply; the padding never enters the counters.
+    """
+
+    parallel = True
+
+    def __init__(self, layout: RankLayout, dist_groups=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.layout = layout
+        self.counters = CommCounters()
+        grid = layout.grid
+        if dist_groups is None:
+            dist_groups = make_slice_process_groups(grid)
+        self.slice_pg = [dist_groups[n][c] for n, c in enumerate(layout.coord)]
+
+    def all_reduce(self, t, op="sum"):
+        if op != "sum":
+            raise ValueError(f"only sum reductions are on this path, got {op!r}")
+        self.dist.all_reduce(t)
+        self.counters.record("AllReduce", t.numel(), t.numel())
+        return t
+
+    def reduce_scatter(self, mode, t, parts):
+        group = self.layout.groups[mode]
+        me = group.index[self.layout.rank]
+        r = int(t.shape[1])
+        width = parts.max_length
+        if group.size == 1:
+            out = t
+        else:
+            if all(x == width for x in parts.lengths):
+                inp = t.reshape(-1)
+            else:
+                inp = torch.zeros((group.size, width, r), dtype=t.dtype, device=t.device)
+                for k in range(group.size):
+                    blk = parts.block(k)
+                    inp[k, : blk.stop - blk.start] = t[blk]
+                inp = inp.reshape(-1)
+            out_full = torch.empty((width, r), dtype=t.dtype, device=t.device)
+            self.dist.reduce_scatter_tensor(out_full.reshape(-1), inp.contiguous(), group=self.slice_pg[mode])
+            out = out_full[: parts.lengths[me]]
+        self.counters.record("ReduceScatter", t.numel(), out.numel())
+        return out
+
+    def all_gather(self, mode, t, parts):
+        group = self.layout.groups[mode]
+        r = int(t.shape[1])
+        width = parts.max_length
+        if group.size == 1:
+            out = t
+        else:
+            src = torch.zeros((width, r), dtype=t.dtype, device=t.device)
+            src[: t.shape[0]] = t
+            full = torch.empty((group.size, width, r), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(full.reshape(-1), src.reshape(-1), group=self.slice_pg[mode])
+            out = torch.cat([full[k, : parts.lengths[k]] for k in range(group.size)], dim=0)
+        self.counters.record("AllGather", t.numel(), out.numel())
+        return out
+
+
+def make_slice_process_groups(grid: Grid):
+    """One torch.distributed group per (mode, coordinate); every rank creates all of them."""
+    import torch.distributed as dist
+
+    groups = []
+    for n in range(len(grid.shape)):
+        per = []
+        for c in range(grid.shape[n]):
+            ranks = list(grid.slice_group(n, c).ranks)
+            per.append(dist.new_group(ranks) if len(ranks) > 1 else None)
+        groups.append(per)
+    return groups
+
+
+class _Rendezvous:
+    """post -> barrier -> combine -> barrier (grid.py:96-113), with the combine
+    step run between the barriers so device reads finish before slots change."""
+
+    def __init__(self, size: int):
+        self.slots = [None] * size
+        self._enter = threading.Barrier(size)
+        self._leave = threading.Barrier(size)
+
+    def exchange(self, index: int, value, combine):
+        self.slots[index] = value
+        self._enter.wait()
+        out = combine(list(self.slots))
+        self._leave.wait()
+        return out
+
+    def abort(self):
+        self._enter.abort()
+        self._leave.abort()
+
+
+class ThreadGrid:
+    """Shared state of a thread-simulated grid (one rendezvous per group)."""
+
+    def __init__(self, grid: Grid):
+        self.grid = grid
+        self.all_rv = _Rendezvous(grid.total)
+        self.slice_rv = [[_Rendezvous(g.size) for g in per] for per in grid.slice_groups]
+
+    def abort(self):
+        self.all_rv.abort()
+        for per in self.slice_rv:
+            for rv in per:
+                rv.abort()
+
+
+class ThreadCollectives:
+    """Rank-ordered collectives between worker threads on the local device(s)."""
+
+    parallel = True
+
+    def __init__(self, tgrid: ThreadGrid, layout: RankLayout):
+        self.tgrid = tgrid
+        self.layout = layout
+        self.counters = CommCounters()
+
+    @staticmethod
+    def _sync():
+        torch.cuda.current_stream().synchronize()
+
+    def all_reduce(self, t, op="sum"):
+        if op != "sum":
+            raise ValueError(f"only sum reductions are on this path, got {op!r}")
+        self._sync()
+
+        def combine(slots):
+            out = slots[0].clone()
+            for s in slots[1:]:
+                out += s
+            self._sync()
+            return out
+
+        out = self.tgrid.all_rv.exchange(self.layout.rank, t, combine)
+        t.copy_(out)
+        self.counters.record("AllReduce", t.numel(), t.numel())
+        return t
+
+    def reduce_scatter(self, mode, t, parts):
+        group = self.layout.groups[mode]
+        me = group.index[self.layout.rank]
+        rv = self.tgrid.slice_rv[mode][self.layout.coord[mode]]
+        self._sync()
+
+        def combine(slots):
+            blk = parts.block(me)
+            out = slots[0][blk].clone()
+            for s in slots[1:]:
+                out += s[blk]
+            self._sync()
+            return out
+
+        out = rv.exchange(me, t, combine)
+        self.counters.record("ReduceScatter", t.numel(), out.numel())
+        return out
+
+    def all_gather(self, mode, t, parts):
+        group = self.layout.groups[mode]
+        me = group.index[self.layout.rank]
+        rv = self.tgrid.slice_rv[mode][self.layout.coord[mode]]
+        self._sync()
+
+        def combine(slots):
+            out = torch.cat(slots, dim=0)
+            self._sync()
+            return out
+
+        out = rv.exchange(me, t, combine)
+        self.counters.record("AllGather", t.numel(), out.numel())
+        return out

@@ -1,0 +1,49 @@
+"""The C-ABI library loads on a CPU-only host and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+from tests.conftest import ROOT
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "nncp_b200.h")).read()
+    return sorted(set(re.findall(r"\b(nncp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_header_symbols():
+    from paper_1909_01149_b200 import _lib
+
+    lib = _lib.load(require_device=False)
+    names = _declared()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    bound = {n for n, _, _ in _lib.SIGNATURES}
+    assert bound == set(names)
+
+
+def test_pure_host_entry_points():
+    from paper_1909_01149_b200 import _lib
+
+    lib = _lib.load(require_device=False)
+    assert lib.nncp_abi_version() == 1
+    out = ctypes.c_int(0)
+    assert lib.nncp_choose_split(3, _lib.i64([128, 128, 128]), 0, ctypes.byref(out)) == 0 and out.value == 2
+    assert lib.nncp_choose_split(4, _lib.i64([384] * 4), 1, ctypes.byref(out)) == 0 and out.value == 3
+    assert lib.nncp_choose_split(3, _lib.i64([1446680, 69, 25]), 0, ctypes.byref(out)) == 0 and out.value == 1
+    assert lib.nncp_choose_split(3, _lib.i64([2, 2, 100]), 0, ctypes.byref(out)) == 0 and out.value == 2
+    assert lib.nncp_workspace_bytes(3, _lib.i64([2048] * 3), 2, 32) > 0
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import pytest
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1909_01149_b200 as P
+
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        P.gram([[1.0, 2.0], [3.0, 4.0]])

@@ -1,0 +1,294 @@
+"""CUDA path vs the reference (golden vectors from the live reference) and vs
+the CPU oracle.  Tolerances are BASELINE.json's north star: single MTTKRP /
+Gram <= 1e-12 relative Frobenius, error trace <= 1e-9 over the first 10
+iterations, final column-normalised factors <= 1e-6."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import nncp_oracle as O
+from tests.conftest import rel_fro
+
+pytestmark = pytest.mark.gpu
+
+MTTKRP_TOL = 1e-12
+TRACE_TOL = 1e-9
+FACTOR_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1909_01149_b200 as pkg
+
+    return pkg
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def test_library_is_the_product(P):
+    from paper_1909_01149_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.nncp_abi_version() == 1
+    assert lib.nncp_device_sms() == 148
+
+
+def test_partials_and_ttv_vs_golden(P, golden):
+    g = golden("mttkrp.npz")
+    for k in range(int(g["ncases"])):
+        dims = tuple(int(d) for d in g[f"c{k}_dims"])
+        r = int(g[f"c{k}_rank"])
+        x = P.DenseTensor(dims, g[f"c{k}_x"])
+        hs = [g[f"c{k}_h{n}"] for n in range(len(dims))]
+        plan = P.DimTreePlan.create(dims, r)
+        assert plan.split == int(g[f"c{k}_split"])
+        tl = P.partial_mttkrp(x, hs, "left", plan)
+        tr = P.partial_mttkrp(x, hs, "right", plan)
+        assert rel_fro(_np(tl.data), g[f"c{k}_tl"]) <= MTTKRP_TOL, k
+        assert rel_fro(_np(tr.data), g[f"c{k}_tr"]) <= MTTKRP_TOL, k
+        s = plan.split
+        if s >= 2:
+            trail = P.multi_ttv(tl, hs[1:s], "trailing")
+            lead = P.multi_ttv(tl, hs[0], "leading")
+            assert rel_fro(_np(trail.data), g[f"c{k}_ttv_trail"]) <= MTTKRP_TOL, k
+            assert rel_fro(_np(lead.data), g[f"c{k}_ttv_lead"]) <= MTTKRP_TOL, k
+
+
+def test_dimtree_all_modes_vs_golden(P, golden):
+    g = golden("mttkrp.npz")
+    for k in range(int(g["ncases"])):
+        dims = tuple(int(d) for d in g[f"c{k}_dims"])
+        r = int(g[f"c{k}_rank"])
+        x = P.DenseTensor(dims, g[f"c{k}_x"]).to_device()
+        hs = [g[f"c{k}_h{n}"] for n in range(len(dims))]
+        ctx = P.DimTreeContext(P.DimTreePlan.create(dims, r))
+        ctx.begin_iteration()
+        cur = list(hs)
+        for n in range(len(dims)):
+            got = _np(ctx.mttkrp(x, cur, n))
+            assert rel_fro(got, g[f"c{k}_m{n}"]) <= MTTKRP_TOL, (k, n)
+            cur[n] = g[f"c{k}_new{n}"]
+        assert ctx.partial_calls == 2
+        last = _np(P.DimTreeContext(P.DimTreePlan.create(dims, r)).mttkrp_last_mode(x, hs))
+        assert rel_fro(last, g[f"c{k}_last"]) <= MTTKRP_TOL
+        assert rel_fro(last, g[f"c{k}_naive_last"]) <= MTTKRP_TOL
+
+
+def test_dimtree_order_errors(P):
+    x = P.DenseTensor((2, 2, 2), np.ones(8)).to_device()
+    hs = [np.ones((2, 1))] * 3
+    ctx = P.DimTreeContext(P.DimTreePlan.create((2, 2, 2), 1))
+    with pytest.raises(RuntimeError):
+        ctx.mttkrp(x, hs, 0)
+    ctx.begin_iteration()
+    with pytest.raises(RuntimeError):
+        ctx.mttkrp(x, hs, 1)
+
+
+@pytest.mark.parametrize("dims,r", [((128, 96, 80), 32), ((64, 48, 40, 24), 16), ((4096, 64, 32), 20),
+                                    ((100, 64, 64), 64), ((256, 256, 300), 8), ((7, 9, 11), 5)])
+def test_partials_vs_oracle_larger(P, dims, r):
+    rng = np.random.default_rng(sum(dims) + r)
+    x = rng.random(int(np.prod(dims)))
+    hs = [rng.random((d, r)) for d in dims]
+    plan = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    for side, fn in (("left", O.partial_left), ("right", O.partial_right)):
+        got = _np(P.partial_mttkrp(xd, hs, side, plan).data)
+        want = fn(x, dims, plan.split, hs)
+        assert rel_fro(got, want) <= MTTKRP_TOL, side
+
+
+def test_updates_vs_golden(P, golden):
+    g = golden("updates.npz")
+    for k in range(int(g["nupd"])):
+        inp = P.UpdateInputs(g[f"u{k}_s"], g[f"u{k}_m"], g[f"u{k}_cur"])
+        assert rel_fro(_np(P.mu_update(inp)), g[f"u{k}_mu"]) <= 1e-13, k
+        assert rel_fro(_np(P.hals_update(inp)), g[f"u{k}_hals"]) <= 1e-12, k
+        got = _np(P.bpp_update(inp))
+        assert np.allclose(got, g[f"u{k}_bpp"], rtol=1e-9, atol=1e-11), k
+
+
+def test_hals_zero_diagonal_and_bpp_cycling(P, golden):
+    g = golden("updates.npz")
+    with pytest.warns(UserWarning):
+        out = P.hals_update(P.UpdateInputs(g["hals_zero_s"], g["hals_zero_m"], g["hals_zero_cur"]))
+    assert np.array_equal(_np(out), g["hals_zero_out"])
+    with pytest.raises(P.BppCyclingError) as info:
+        P.bpp_update(P.UpdateInputs(g["bpp_cycle_s"], g["bpp_cycle_m"], np.zeros((2, 2))))
+    assert info.value.column == 1
+
+
+def test_bpp_matches_enumeration(P):
+    rng = np.random.default_rng(105)
+    for _ in range(30):
+        r = int(rng.integers(1, 9))
+        a = rng.standard_normal((r + 4, r))
+        s = a.T @ a
+        f = rng.standard_normal((3, r)) * 2.0
+        got = _np(P.bpp_update(P.UpdateInputs(s, f, np.zeros_like(f))))
+        want = O.bpp_update(s, f)
+        assert np.allclose(got, want, atol=1e-8)
+        assert (got >= 0).all()
+
+
+def test_gram_and_inner(P):
+    rng = np.random.default_rng(5)
+    h = rng.random((1000, 24))
+    assert rel_fro(_np(P.gram(h)), O.gram(h)) <= MTTKRP_TOL
+    a, b = rng.random((50, 7)), rng.random((50, 7))
+    assert abs(P.matrix_inner_product(a, b) - float(np.sum(a * b))) <= 1e-12 * float(np.sum(a * b))
+    x = P.DenseTensor((30, 20, 10), rng.random(6000))
+    assert abs(P.norm_squared(x) - float(x.data @ x.data)) <= 1e-13 * float(x.data @ x.data)
+
+
+def _run_case(P, g, name, **extra):
+    dims = tuple(int(d) for d in g[f"{name}_dims"])
+    r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
+    algo = str(g[f"{name}_algo"])
+    x = P.DenseTensor(dims, g[f"{name}_x"])
+    cfg = P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed, **extra)
+    return dims, r, iters, algo, x, cfg
+
+
+def test_sequential_runs_vs_golden(P, golden):
+    g = golden("runs.npz")
+    for name in [str(n) for n in g["names"]]:
+        dims, r, iters, algo, x, cfg = _run_case(P, g, name)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            rep = P.nncp_sequential(x, cfg)
+        ref = g[f"{name}_errors"]
+        got = np.array(rep.errors)
+        assert len(got) == len(ref)
+        k = min(11, len(ref))
+        assert np.max(np.abs(got[:k] - ref[:k])) <= TRACE_TOL, (name, np.max(np.abs(got[:k] - ref[:k])))
+        for n in range(len(dims)):
+            assert np.max(np.abs(rep.model.factors[n] - g[f"{name}_f{n}"])) <= FACTOR_TOL, (name, n)
+        assert rel_fro(rep.model.lam, g[f"{name}_lam"]) <= FACTOR_TOL
+        assert rep.split_mode == int(g[f"{name}_split"])
+        assert rep.tree_partial_calls == 2 * iters
+        for h in rep.model.factors:
+            norms = np.linalg.norm(h, axis=0)
+            assert np.all((np.abs(norms - 1.0) < 1e-12) | (norms == 0.0))
+
+
+def test_cuda_graph_matches_eager(P, golden):
+    g = golden("runs.npz")
+    for name in ("c1_mu", "hals_r16", "bpp4"):
+        _, _, _, _, x, cfg = _run_case(P, g, name)
+        eager = P.nncp_sequential(x, cfg)
+        _, _, _, _, x, cfg = _run_case(P, g, name, cuda_graph=True)
+        graph = P.nncp_sequential(x, cfg)
+        assert eager.errors == graph.errors, name
+        for a, b in zip(eager.model.factors, graph.model.factors):
+            assert np.array_equal(a, b)
+        assert graph.tree_partial_calls == eager.tree_partial_calls
+
+
+def test_run_to_run_determinism(P, golden):
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, "bpp_r32")
+    a = P.nncp_sequential(x, cfg)
+    b = P.nncp_sequential(x, cfg)
+    assert a.errors == b.errors
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+
+
+def test_no_dimtree_matches_tree(P, golden):
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, "mu4")
+    tree = P.nncp_sequential(x, cfg)
+    _, _, _, _, x, cfg = _run_case(P, g, "mu4", use_dimtree=False)
+    flat = P.nncp_sequential(x, cfg)
+    assert np.allclose(tree.errors, flat.errors, rtol=0, atol=1e-12)
+    assert flat.tree_partial_calls == 0
+
+
+def test_grid_runs_vs_golden(P, golden):
+    g = golden("runs.npz")
+    for tag in [str(t) for t in g["grids"]]:
+        name = tag[len("grid_"):tag.rindex("_")]
+        grid = tuple(int(v) for v in tag[tag.rindex("_") + 1:].split("x"))
+        dims, r, iters, algo, x, cfg = _run_case(P, g, name, grid=grid)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            par = P.nncp_parallel(x, cfg)
+        ref = g[f"{tag}_errors"]
+        assert np.max(np.abs(np.array(par.errors) - ref)) <= 1e-9, tag
+        assert par.split_mode == int(g[f"{tag}_split"])
+        for n in range(len(dims)):
+            assert np.max(np.abs(par.model.factors[n] - g[f"{tag}_f{n}"])) <= FACTOR_TOL, (tag, n)
+        calls = [par.counters.calls.get(c, 0) for c in ("ReduceScatter", "AllGather", "AllReduce")]
+        ref_calls = list(g[f"{tag}_calls"])
+        assert calls[:2] == ref_calls[:2], tag
+        if algo != "hals":  # the reference's per-column HALS hook All-Reduce is elided here
+            assert calls[2] == ref_calls[2], tag
+            assert [par.counters.words_in.get(c, 0) for c in ("ReduceScatter", "AllGather", "AllReduce")] == \
+                list(g[f"{tag}_words_in"]), tag
+
+
+def test_trivial_grid_bitwise_equals_sequential(P, golden):
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, "bpp3")
+    seq = P.nncp_sequential(x, cfg)
+    _, _, _, _, x, cfg = _run_case(P, g, "bpp3", grid=(1, 1, 1))
+    par = P.nncp_parallel(x, cfg)
+    assert seq.errors == par.errors
+    for a, b in zip(seq.model.factors, par.model.factors):
+        assert np.array_equal(a, b)
+
+
+def test_errors_and_validation(P):
+    x = P.DenseTensor((3, 3), np.ones(9))
+    with pytest.raises(ValueError):
+        P.nncp_sequential(x, P.RunConfig(rank=0, max_iters=1))
+    with pytest.raises(ValueError):
+        P.nncp_sequential(x, P.RunConfig(rank=1, algorithm="sgd"))
+    with pytest.raises(ValueError, match="zero tensor"):
+        P.nncp_sequential(P.DenseTensor((3, 3)), P.RunConfig(rank=1, algorithm="mu", max_iters=1))
+    with pytest.warns(UserWarning, match="negative"):
+        P.nncp_sequential(P.DenseTensor((3, 3), -np.ones(9)), P.RunConfig(rank=1, algorithm="mu", max_iters=1,
+                                                                          tol=0.0))
+    with pytest.raises(ValueError, match="exceeds tensor dim"):
+        P.nncp_parallel(P.DenseTensor((5, 3, 4), np.ones(60)), P.RunConfig(rank=2, grid=(1, 5, 1)))
+
+
+def test_exact_init_is_fixed_point_bpp(P):
+    rng = np.random.default_rng(3)
+    hs = [rng.random((d, 2)) + 0.05 for d in (5, 4, 3)]
+    normed, lam = [], np.ones(2)
+    for h in hs:
+        hn, w = O.normalize_columns(h)
+        normed.append(hn)
+        lam = lam * w
+    x = P.DenseTensor((5, 4, 3), O.reconstruct(normed, lam))
+    cfg = P.RunConfig(rank=2, algorithm="bpp", max_iters=1, tol=0.0,
+                      initial_factors=P.FactorSet(normed, lam))
+    rep = P.nncp_sequential(x, cfg)
+    assert rep.errors[0] <= 1e-7 and rep.errors[1] <= 1e-7
+
+
+def test_synthetic_blocks_match_global(P):
+    import torch
+
+    dims, r = (40, 30, 20), 6
+    fs = P.truth_factors(dims, r, seed=3)
+    from paper_1909_01149_b200.synth import synthetic_block
+
+    full = _np(synthetic_block(dims, fs, 0.05, 3)).reshape(dims, order="F")
+    assert (full >= 0).all()
+    blk = _np(synthetic_block(dims, fs, 0.05, 3, offsets=(10, 0, 5), local_dims=(20, 30, 7)))
+    assert np.array_equal(blk.reshape((20, 30, 7), order="F"), full[10:30, :, 5:12])
+    clean = O.reconstruct(fs, np.ones(r)).reshape(dims, order="F")
+    assert np.all(full >= clean - 1e-12)
+    torch.cuda.synchronize()
