@@ -63,6 +63,8 @@ int nncp_abi_version(void);
 const char* nncp_last_error(void);
 /* SM count of the current device, for host-side bookkeeping */
 int nncp_device_sms(void);
+/* Number of kernels this library has launched in the process (evidence counter). */
+unsigned long long nncp_launch_count(void);
 
 /* dimtree.py:25-39 choose_split_mode.  dims: host array. */
 int nncp_choose_split(int order, const int64_t* dims, int strict, int* split_out);

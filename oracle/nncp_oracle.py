@@ -115,13 +115,19 @@ def partial_right(data, dims, split, factors) -> np.ndarray:
 def ttv_trailing(temp, lead: int, rank: int, coeff) -> np.ndarray:
     """out[l, r] = sum_j T_r[l, j] coeff[j, r] (dimtree.py:159-165); flat rank slowest."""
     t = temp.reshape((lead, -1, rank), order="F")
-    return np.einsum("ljr,jr->lr", t, coeff).ravel(order="F")
+    out = np.empty((lead, rank), order="F")
+    for r in range(rank):  # one BLAS matvec per rank block, as the reference
+        out[:, r] = t[:, :, r] @ coeff[:, r]
+    return out.ravel(order="F")
 
 
 def ttv_leading(temp, lead: int, rank: int, coeff) -> np.ndarray:
     """out[j, r] = sum_l T_r[l, j] coeff[l, r] (dimtree.py:166-172); flat rank slowest."""
     t = temp.reshape((lead, -1, rank), order="F")
-    return np.einsum("ljr,lr->jr", t, coeff).ravel(order="F")
+    out = np.empty((t.shape[1], rank), order="F")
+    for r in range(rank):
+        out[:, r] = t[:, :, r].T @ coeff[:, r]
+    return out.ravel(order="F")
 
 
 class DimTree:
@@ -285,7 +291,7 @@ def eps_from_terms(alpha, beta, gamma) -> float:
 
 def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, seed=0,
                    use_dimtree=True, strict_split=False, initial_factors=None,
-                   initial_lam=None, timings=None):
+                   initial_lam=None, timings=None, init_error="naive"):
     """Alternating-update NNCP, sequential runtime (driver.py:331-449, 495-505).
 
     Returns (errors, factors, lam, split, partial_calls).  ``timings``, when a
@@ -309,7 +315,10 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
         lam = np.ones(rank)
     grams = [gram(h) for h in hs]
     tree = DimTree(dims, rank, strict_split) if use_dimtree else None
-    m0 = naive_mttkrp(data, dims, hs, order - 1)
+    if init_error == "naive":
+        m0 = naive_mttkrp(data, dims, hs, order - 1)
+    else:  # same quantity through the tree's last-mode path (bench baseline: init is not timed)
+        m0 = DimTree(dims, rank, strict_split).mttkrp_last_mode(data, hs)
     beta0 = float(np.dot(m0.ravel(), (hs[-1] * lam).ravel()))
     gamma0 = float(lam @ (np.prod(grams, axis=0) @ lam))
     errors = [eps_from_terms(alpha, beta0, gamma0)]

@@ -35,6 +35,7 @@ SIGNATURES = [
     ("nncp_abi_version", ctypes.c_int, []),
     ("nncp_last_error", ctypes.c_char_p, []),
     ("nncp_device_sms", ctypes.c_int, []),
+    ("nncp_launch_count", ctypes.c_ulonglong, []),
     ("nncp_choose_split", ctypes.c_int, [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("nncp_workspace_bytes", ctypes.c_size_t, [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int]),
     ("nncp_norm_squared", ctypes.c_int, [vp, ctypes.c_int64, vp, vp, ctypes.c_size_t, vp]),

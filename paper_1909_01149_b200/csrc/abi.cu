@@ -1,6 +1,7 @@
 // extern "C" boundary (include/nncp_b200.h): argument validation, error
 // reporting and dispatch to the kernels.  Validation messages mirror the
 // reference's ValueError / RuntimeError texts where one exists.
+#include <atomic>
 #include <string>
 
 #include "common.cuh"
@@ -8,6 +9,8 @@
 namespace nncp {
 
 thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
@@ -55,6 +58,7 @@ extern "C" {
 int nncp_abi_version(void) { return NNCP_ABI_VERSION; }
 const char* nncp_last_error(void) { return g_last_error.c_str(); }
 int nncp_device_sms(void) { return num_sms(); }
+unsigned long long nncp_launch_count(void) { return g_launches.load(); }
 
 int nncp_choose_split(int order, const int64_t* dims, int strict, int* split_out) {
   if (order < 2) return fail(NNCP_ERR_VALUE, "need at least 2 modes");

@@ -28,7 +28,12 @@ int fail(int code, const std::string& msg);
       return ::nncp::fail(NNCP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-#define NNCP_LAUNCH_CHECK() NNCP_CUDA_TRY(cudaGetLastError())
+void count_launch();
+#define NNCP_LAUNCH_CHECK()            \
+  do {                                 \
+    ::nncp::count_launch();            \
+    NNCP_CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 constexpr int kMaxOrder = NNCP_MAX_ORDER;
 constexpr int kMaxRank = NNCP_MAX_RANK;

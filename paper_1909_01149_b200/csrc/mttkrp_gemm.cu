@@ -39,6 +39,93 @@ __device__ __forceinline__ double krp_value(const KrpSpec& s, int64_t k, int r, 
   return v * __ldg(s.ptr[s.n - 1] + k * R + r);
 }
 
+
+// Per-lane cursor over the U Khatri-Rao rows a producer lane fills in every stage.
+// Row k is kept both linear (for the range check) and as its mixed-radix digits
+// (first factor fastest), advanced by a fixed stride per stage: no 64-bit
+// divisions in the steady state, so every factor load of a stage can be issued
+// back to back (one L2 round trip per stage).
+template <int U, int NFM>
+struct KrpCursor {
+  int64_t k[U];
+  uint32_t dig[U][NFM];
+
+  // factor count: compile-time when the launcher dispatched an exact NFM (1 or 2)
+  __device__ __forceinline__ static int count(const KrpSpec& s) { return NFM <= 2 ? NFM : s.n; }
+
+  template <class IdxFn>
+  __device__ __forceinline__ void init(const KrpSpec& s, IdxFn idx_of, int c) {
+    const int n = count(s);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      k[u] = idx_of(u, c);
+      int64_t q = k[u];
+#pragma unroll
+      for (int f = 0; f < NFM; ++f) {
+        const bool act = f < n, last = f == n - 1;
+        const int64_t d = (act && !last) ? s.dim[f] : 1;
+        const int64_t r = q % d;
+        dig[u][f] = act ? uint32_t(last ? q : r) : 0u;
+        q = (act && !last) ? q / d : q;
+      }
+    }
+  }
+
+  __device__ __forceinline__ void advance(const KrpSpec& s, uint32_t step) {
+    const int n = count(s);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      k[u] += step;
+      uint32_t carry = step;
+#pragma unroll
+      for (int f = 0; f < NFM; ++f) {
+        const bool act = f < n, last = f == n - 1;
+        uint32_t v = dig[u][f] + carry;
+        carry = 0;
+        if (act && !last) {
+          const uint32_t d = uint32_t(s.dim[f]);
+          if (v >= d) {
+            carry = v / d;
+            v -= carry * d;
+          }
+        }
+        dig[u][f] = act ? v : 0u;
+      }
+    }
+  }
+};
+
+// One pipeline stage of fragment-native Khatri-Rao values: for k4-step u < U and
+// n-fragment j < NF, lane (g, c) writes KRP[row(u, c)][8j + g] (zero when the row
+// is >= hi or the column >= R).  Multiplication order ((H_a * H_b) * H_c) is
+// khatri_rao's (tensor_ops.py:121-137).
+template <int NF, int U, int NFM>
+__device__ __forceinline__ void produce_krp(const KrpSpec& krp, const KrpCursor<U, NFM>& cur,
+                                            double* __restrict__ bdst, int lane, int R, int64_t hi) {
+  const int g = lane >> 2;
+  double v[U][NF];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool in = cur.k[u] < hi;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) v[u][j] = 1.0;
+#pragma unroll
+    for (int f = 0; f < NFM; ++f) {
+      if (f < KrpCursor<U, NFM>::count(krp)) {
+        const double* base = krp.ptr[f] + (in ? int64_t(cur.dig[u][f]) * R : 0);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) v[u][j] *= __ldg(base + min(8 * j + g, R - 1));
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool in = cur.k[u] < hi;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) bdst[(u * NF + j) * 32 + lane] = (in && 8 * j + g < R) ? v[u][j] : 0.0;
+  }
+}
+
 // ------------------------------------------------------------ left side ----
 template <int RP>
 struct LeftTile {
@@ -52,7 +139,7 @@ struct LeftTile {
   static_assert(size_t(RP) * BM * 8 <= size_t(STAGES) * A_ELEMS * 8, "epilogue tile must fit");
 };
 
-template <int RP>
+template <int RP, int NFM>
 __global__ void __launch_bounds__(288, 1)
     mttkrp_left_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                     const int64_t K, const int64_t k_per_split, double* __restrict__ out,
@@ -74,7 +161,7 @@ __global__ void __launch_bounds__(288, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 33);  // 32 producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
@@ -84,31 +171,23 @@ __global__ void __launch_bounds__(288, 1)
 
   if (warp == 8) {
     // ---------------- producer: TMA for X, on-the-fly KRP rows for B ----------
+    KrpCursor<BK / 4, NFM> cur;
+    cur.init(krp, [&](int t, int cc) { return kb + 4 * t + cc; }, lane & 3);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch % ST;
       if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
       const int64_t k0 = kb + int64_t(ch) * BK;
       if (lane == 0) {
-        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
-                     "r"(uint32_t(T::A_ELEMS * 8))
-                     : "memory");
+        // one arrival that also arms the transaction count, ordered before the copy
+        mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
         tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(m0), int(k0));
       }
-      double* bdst = Bs + s * T::B_ELEMS;
-#pragma unroll
-      for (int t = 0; t < BK / 4; ++t) {
-        const int64_t k = k0 + 4 * t + c;
-        const bool kin = k < ke;
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          const int r = 8 * j + g;
-          double v = 0.0;
-          if (kin && r < R) v = krp_value(krp, k, r, R);
-          bdst[(t * NF + j) * 32 + lane] = v;
-        }
-      }
+      produce_krp<NF, BK / 4, NFM>(krp, cur, Bs + s * T::B_ELEMS, lane, R, ke);
+      cur.advance(krp, BK);
       mbar_arrive(&full[s]);
     }
+    // producer tail: stay resident until the consumers released every stage
+    for (int ch = max(0, nchunks - ST); ch < nchunks; ++ch) mbar_wait(&empty[ch % ST], (ch / ST) & 1);
     return;
   }
 
@@ -141,6 +220,11 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
         for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], a[f], b[j]);
     }
+    // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
+    // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
+    // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
+    // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -179,7 +263,7 @@ struct RightTile {
   static_assert(size_t(RP) * BJ * 8 <= size_t(STAGES) * A_ELEMS * 8, "epilogue tile must fit");
 };
 
-template <int RP>
+template <int RP, int NFM>
 __global__ void __launch_bounds__(288, 1)
     mttkrp_right_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                      const int64_t J, const int64_t m_per_split, double* __restrict__ out,
@@ -201,7 +285,7 @@ __global__ void __launch_bounds__(288, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 33);  // 32 producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
@@ -210,32 +294,24 @@ __global__ void __launch_bounds__(288, 1)
   __syncthreads();
 
   if (warp == 8) {
+    KrpCursor<T::KSTEPS, NFM> cur;
+    cur.init(krp, [&](int u, int cc) { return mb + 8 * (u >> 1) + 2 * cc + (u & 1); }, lane & 3);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch % ST;
       if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
       const int64_t mc = mb + int64_t(ch) * BMC;
       if (lane == 0) {
-        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
-                     "r"(uint32_t(T::A_ELEMS * 8))
-                     : "memory");
+        // one arrival that also arms the transaction count, ordered before the copy
+        mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
         tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(mc), int(j0));
       }
-      double* bdst = Bs + s * T::B_ELEMS;
-#pragma unroll
-      for (int u = 0; u < T::KSTEPS; ++u) {
-        // k4-step u: fragment column c <-> m = 8 (u/2) + 2c + (u&1)
-        const int64_t m = mc + 8 * (u >> 1) + 2 * c + (u & 1);
-        const bool min_ = m < me;
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          const int r = 8 * j + g;
-          double v = 0.0;
-          if (min_ && r < R) v = krp_value(krp, m, r, R);
-          bdst[(u * NF + j) * 32 + lane] = v;
-        }
-      }
+      // k4-step u: fragment column c <-> m = 8 (u/2) + 2c + (u&1)
+      produce_krp<NF, T::KSTEPS, NFM>(krp, cur, Bs + s * T::B_ELEMS, lane, R, me);
+      cur.advance(krp, BMC);
       mbar_arrive(&full[s]);
     }
+    // producer tail: stay resident until the consumers released every stage
+    for (int ch = max(0, nchunks - ST); ch < nchunks; ++ch) mbar_wait(&empty[ch % ST], (ch / ST) & 1);
     return;
   }
 
@@ -272,6 +348,11 @@ __global__ void __launch_bounds__(288, 1)
           dmma884(acc[f][j][0], acc[f][j][1], ahi[f], bhi[j]);
         }
     }
+    // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
+    // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
+    // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
+    // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -422,36 +503,54 @@ PartialPlan plan_partial(int order, const int64_t* dims, int split, int side, in
   return p;
 }
 
-template <int RP>
-int launch_left(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
-                int R, cudaStream_t st) {
+template <int RP, int NFM>
+int launch_left_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
+                   int R, cudaStream_t st) {
   using T = LeftTile<RP>;
   static bool attr = false;
   if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_left_tma<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_left_tma<RP, NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(T::SMEM)));
     attr = true;
   }
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_left_tma<RP><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  mttkrp_left_tma<RP, NFM><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+template <int RP, int NFM>
+int launch_right_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
+                    int R, cudaStream_t st) {
+  using T = RightTile<RP>;
+  static bool attr = false;
+  if (!attr) {
+    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_right_tma<RP, NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(T::SMEM)));
+    attr = true;
+  }
+  dim3 grid(unsigned(p.tiles), unsigned(p.splits));
+  mttkrp_right_tma<RP, NFM><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
 
 template <int RP>
+int launch_left(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride, int R,
+                cudaStream_t st) {
+  if (krp.n == 1) return launch_left_nf<RP, 1>(map, krp, p, dst, stride, R, st);
+  if (krp.n == 2) return launch_left_nf<RP, 2>(map, krp, p, dst, stride, R, st);
+  if (krp.n <= 4) return launch_left_nf<RP, 4>(map, krp, p, dst, stride, R, st);
+  return launch_left_nf<RP, kMaxOrder>(map, krp, p, dst, stride, R, st);
+}
+
+template <int RP>
 int launch_right(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
                  int R, cudaStream_t st) {
-  using T = RightTile<RP>;
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_right_tma<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(T::SMEM)));
-    attr = true;
-  }
-  dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_right_tma<RP><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
-  NNCP_LAUNCH_CHECK();
-  return NNCP_OK;
+  if (krp.n == 1) return launch_right_nf<RP, 1>(map, krp, p, dst, stride, R, st);
+  if (krp.n == 2) return launch_right_nf<RP, 2>(map, krp, p, dst, stride, R, st);
+  if (krp.n <= 4) return launch_right_nf<RP, 4>(map, krp, p, dst, stride, R, st);
+  return launch_right_nf<RP, kMaxOrder>(map, krp, p, dst, stride, R, st);
 }
 
 #define NNCP_RP_DISPATCH(RPV, FN, ...)                  \

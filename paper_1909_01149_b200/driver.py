@@ -364,12 +364,14 @@ class _Engine:
         beta, gamma = self.host_scal.tolist()
         return _eps_from_terms(self.alpha, beta, gamma)
 
-    def iterate(self):
+    def iterate(self, count: int = None):
+        """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
         cfg = self.cfg
         errors = self.report.errors
         use_graph = cfg.cuda_graph and not self.coll.parallel
-        converged = False
-        for it in range(1, cfg.max_iters + 1):
+        done = len(errors) - 1
+        stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
+        for it in range(done + 1, stop + 1):
             self.report.begin_row()
             wall0 = time.perf_counter()
             if use_graph and self.graph is None and it > 1:
@@ -387,9 +389,8 @@ class _Engine:
             self.report.row_wall[-1] = time.perf_counter() - wall0
             self.report.row_words[-1] = self.coll.counters.total_words() - sum(self.report.row_words[:-1])
             if eps <= cfg.tol:
-                converged = True
+                self.report.converged = True
                 break
-        self.report.converged = converged
         self.report.tree_partial_calls = self.ctx.partial_calls if cfg.use_dimtree else 0
 
     def _capture(self):

@@ -292,3 +292,19 @@ def test_synthetic_blocks_match_global(P):
     clean = O.reconstruct(fs, np.ones(r)).reshape(dims, order="F")
     assert np.all(full >= clean - 1e-12)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dims,r", [((256, 256, 304), 8), ((256, 256, 300), 32), ((512, 512, 64), 16)])
+def test_partials_bitwise_reproducible_multiwave(P, dims, r):
+    """Regression: a stage refill used to race the consumers' last ld.shared (multi-wave grids)."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    x = rng.random(int(np.prod(dims)))
+    hs = [torch.from_numpy(rng.random((d, r))).cuda() for d in dims]
+    plan = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    for side in ("left", "right"):
+        first = P.partial_mttkrp(xd, hs, side, plan).data.clone()
+        for _ in range(15):
+            assert torch.equal(P.partial_mttkrp(xd, hs, side, plan).data, first), side
