@@ -126,6 +126,11 @@ __device__ __forceinline__ void produce_krp(const KrpSpec& krp, const KrpCursor<
   }
 }
 
+// Producer warps per CTA: each generates 1/kProducers of every stage's KRP rows
+// (the right partial's 2-factor rows saturated a single producer warp).
+constexpr int kProducers = 2;
+constexpr int kThreads = 256 + 32 * kProducers;
+
 // ------------------------------------------------------------ left side ----
 template <int RP>
 struct LeftTile {
@@ -140,7 +145,7 @@ struct LeftTile {
 };
 
 template <int RP, int NFM>
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     mttkrp_left_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                     const int64_t K, const int64_t k_per_split, double* __restrict__ out,
                     const int64_t split_stride, const int R) {
@@ -161,28 +166,30 @@ __global__ void __launch_bounds__(288, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 33);  // 32 producer lanes + the expect_tx arrival
+      mbar_init(&full[s], 32 * kProducers + 1);  // producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
   }
   if (warp == 8 && lane == 0) prefetch_tma_desc(&xmap);
+  const int pw = warp - 8;  // producer warp index (>= 0 for producers)
   __syncthreads();
 
-  if (warp == 8) {
-    // ---------------- producer: TMA for X, on-the-fly KRP rows for B ----------
-    KrpCursor<BK / 4, NFM> cur;
-    cur.init(krp, [&](int t, int cc) { return kb + 4 * t + cc; }, lane & 3);
+  if (warp >= 8) {
+    // ---------------- producers: TMA for X, on-the-fly KRP rows for B ---------
+    constexpr int UP = BK / 4 / kProducers;
+    KrpCursor<UP, NFM> cur;
+    cur.init(krp, [&](int t, int cc) { return kb + 4 * (t + pw * UP) + cc; }, lane & 3);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch % ST;
       if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
       const int64_t k0 = kb + int64_t(ch) * BK;
-      if (lane == 0) {
+      if (pw == 0 && lane == 0) {
         // one arrival that also arms the transaction count, ordered before the copy
         mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
         tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(m0), int(k0));
       }
-      produce_krp<NF, BK / 4, NFM>(krp, cur, Bs + s * T::B_ELEMS, lane, R, ke);
+      produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, ke);
       cur.advance(krp, BK);
       mbar_arrive(&full[s]);
     }
@@ -264,7 +271,7 @@ struct RightTile {
 };
 
 template <int RP, int NFM>
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     mttkrp_right_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                      const int64_t J, const int64_t m_per_split, double* __restrict__ out,
                      const int64_t split_stride, const int R) {
@@ -285,28 +292,33 @@ __global__ void __launch_bounds__(288, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 33);  // 32 producer lanes + the expect_tx arrival
+      mbar_init(&full[s], 32 * kProducers + 1);  // producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
   }
   if (warp == 8 && lane == 0) prefetch_tma_desc(&xmap);
+  const int pw = warp - 8;  // producer warp index (>= 0 for producers)
   __syncthreads();
 
-  if (warp == 8) {
-    KrpCursor<T::KSTEPS, NFM> cur;
-    cur.init(krp, [&](int u, int cc) { return mb + 8 * (u >> 1) + 2 * cc + (u & 1); }, lane & 3);
+  if (warp >= 8) {
+    constexpr int UP = T::KSTEPS / kProducers;
+    KrpCursor<UP, NFM> cur;
+    cur.init(krp, [&](int u, int cc) {
+      const int uu = u + pw * UP;
+      return mb + 8 * (uu >> 1) + 2 * cc + (uu & 1);
+    }, lane & 3);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch % ST;
       if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
       const int64_t mc = mb + int64_t(ch) * BMC;
-      if (lane == 0) {
+      if (pw == 0 && lane == 0) {
         // one arrival that also arms the transaction count, ordered before the copy
         mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
         tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(mc), int(j0));
       }
       // k4-step u: fragment column c <-> m = 8 (u/2) + 2c + (u&1)
-      produce_krp<NF, T::KSTEPS, NFM>(krp, cur, Bs + s * T::B_ELEMS, lane, R, me);
+      produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, me);
       cur.advance(krp, BMC);
       mbar_arrive(&full[s]);
     }
@@ -514,7 +526,7 @@ int launch_left_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan
     attr = true;
   }
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_left_tma<RP, NFM><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  mttkrp_left_tma<RP, NFM><<<grid, kThreads, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
@@ -530,7 +542,7 @@ int launch_right_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPla
     attr = true;
   }
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_right_tma<RP, NFM><<<grid, 288, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  mttkrp_right_tma<RP, NFM><<<grid, kThreads, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
