@@ -456,24 +456,24 @@ int make_map_2d(CUtensorMap* map, const double* base, uint64_t inner, uint64_t o
 
 }  // namespace
 
-// Split-K chooser: smallest split count whose CTA waves fill >= 95% of the SMs
-// (1 resident CTA per SM), keeping >= 8 pipeline chunks per split.
+// Split-K chooser: the smallest split count whose CTA waves (1 resident CTA per
+// SM) come within 1% of the best achievable SM fill, keeping >= 8 pipeline
+// chunks per split.
 int choose_splits(int64_t tiles, int64_t chunks) {
   const int64_t sms = num_sms();
-  int best = 1;
-  double best_eff = 0.0;
   const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(chunks / 8, 4 * sms));
+  double best_eff = 0.0;
   for (int64_t s = 1; s <= max_s; ++s) {
     const int64_t ctas = tiles * s;
     const int64_t waves = (ctas + sms - 1) / sms;
-    const double eff = double(ctas) / double(waves * sms);
-    if (eff >= 0.95) return int(s);
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = int(s);
-    }
+    best_eff = std::max(best_eff, double(ctas) / double(waves * sms));
   }
-  return best;
+  for (int64_t s = 1; s <= max_s; ++s) {
+    const int64_t ctas = tiles * s;
+    const int64_t waves = (ctas + sms - 1) / sms;
+    if (double(ctas) / double(waves * sms) >= best_eff - 0.01) return int(s);
+  }
+  return 1;
 }
 
 struct PartialPlan {
