@@ -126,10 +126,10 @@ __device__ __forceinline__ void produce_krp(const KrpSpec& krp, const KrpCursor<
   }
 }
 
-// Producer warps per CTA: each generates 1/kProducers of every stage's KRP rows
-// (the right partial's 2-factor rows saturated a single producer warp).
-constexpr int kProducers = 2;
-constexpr int kThreads = 256 + 32 * kProducers;
+// Producer warps per CTA: each generates 1/PRODUCERS of every stage's KRP rows.
+// A producer warp is bound by one L2 round trip per stage (the factor rows do
+// not fit the ~7 KB of L1 left next to the pipeline), so stages are split
+// across warps until the consumers, not the producers, set the pace.
 
 // ------------------------------------------------------------ left side ----
 template <int RP>
@@ -138,6 +138,8 @@ struct LeftTile {
   static constexpr int BK = 16;   // contracted columns per stage
   static constexpr int NF = RP / 8;
   static constexpr int STAGES = (RP <= 32) ? 5 : 4;
+  static constexpr int PRODUCERS = 4;
+  static constexpr int THREADS = 256 + 32 * PRODUCERS;
   static constexpr int A_ELEMS = BM * BK;
   static constexpr int B_ELEMS = BK * RP;
   static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * 8 + 2 * STAGES * 8;
@@ -145,7 +147,7 @@ struct LeftTile {
 };
 
 template <int RP, int NFM>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
     mttkrp_left_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                     const int64_t K, const int64_t k_per_split, double* __restrict__ out,
                     const int64_t split_stride, const int R) {
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32 * kProducers + 1);  // producer lanes + the expect_tx arrival
+      mbar_init(&full[s], 32 * T::PRODUCERS + 1);  // producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= 8) {
     // ---------------- producers: TMA for X, on-the-fly KRP rows for B ---------
-    constexpr int UP = BK / 4 / kProducers;
+    constexpr int UP = BK / 4 / T::PRODUCERS;
+    static_assert(UP * T::PRODUCERS == BK / 4, "stage steps must split evenly");
     KrpCursor<UP, NFM> cur;
     cur.init(krp, [&](int t, int cc) { return kb + 4 * (t + pw * UP) + cc; }, lane & 3);
     for (int ch = 0; ch < nchunks; ++ch) {
@@ -264,6 +267,8 @@ struct RightTile {
   static constexpr int KSTEPS = BMC / 4;
   static constexpr int NF = RP / 8;
   static constexpr int STAGES = (RP <= 32) ? 4 : 3;
+  static constexpr int PRODUCERS = (RP <= 32) ? 6 : 3;
+  static constexpr int THREADS = 256 + 32 * PRODUCERS;
   static constexpr int A_ELEMS = BJ * BMC;
   static constexpr int B_ELEMS = KSTEPS * NF * 32;
   static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * 8 + 2 * STAGES * 8;
@@ -271,7 +276,7 @@ struct RightTile {
 };
 
 template <int RP, int NFM>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
     mttkrp_right_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
                      const int64_t J, const int64_t m_per_split, double* __restrict__ out,
                      const int64_t split_stride, const int R) {
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32 * kProducers + 1);  // producer lanes + the expect_tx arrival
+      mbar_init(&full[s], 32 * T::PRODUCERS + 1);  // producer lanes + the expect_tx arrival
       mbar_init(&empty[s], 8);
     }
     fence_barrier_init();
@@ -302,7 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   if (warp >= 8) {
-    constexpr int UP = T::KSTEPS / kProducers;
+    constexpr int UP = T::KSTEPS / T::PRODUCERS;
+    static_assert(UP * T::PRODUCERS == T::KSTEPS, "stage steps must split evenly");
     KrpCursor<UP, NFM> cur;
     cur.init(krp, [&](int u, int cc) {
       const int uu = u + pw * UP;
@@ -526,7 +532,7 @@ int launch_left_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan
     attr = true;
   }
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_left_tma<RP, NFM><<<grid, kThreads, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  mttkrp_left_tma<RP, NFM><<<grid, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
@@ -542,7 +548,7 @@ int launch_right_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPla
     attr = true;
   }
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_right_tma<RP, NFM><<<grid, kThreads, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  mttkrp_right_tma<RP, NFM><<<grid, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

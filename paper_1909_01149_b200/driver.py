@@ -239,6 +239,8 @@ class _Engine:
         self.timer = _EventTimer(timing)
         self.lib = _lib.load()
         self.graph = None
+        self.graph_kernels = 0      # library kernels captured in the sweep graph
+        self.graph_replays = 0
         self.report = RunReport()
 
     # -- small wrappers -------------------------------------------------------
@@ -378,6 +380,7 @@ class _Engine:
                 self._capture()
             if self.graph is not None:
                 self.graph.replay()
+                self.graph_replays += 1
                 if cfg.use_dimtree:
                     self.ctx.partial_calls += 2
             else:
@@ -398,6 +401,7 @@ class _Engine:
         timing = self.timer.enabled
         self.timer.enabled = False
         calls = self.ctx.partial_calls
+        launches0 = self.lib.nncp_launch_count()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -406,6 +410,7 @@ class _Engine:
                 self._sweep()
         torch.cuda.current_stream().wait_stream(side)
         self.ctx.partial_calls = calls
+        self.graph_kernels = int(self.lib.nncp_launch_count() - launches0)
         self.graph = g
         self.timer.enabled = timing
 
