@@ -308,3 +308,39 @@ def test_partials_bitwise_reproducible_multiwave(P, dims, r):
         first = P.partial_mttkrp(xd, hs, side, plan).data.clone()
         for _ in range(15):
             assert torch.equal(P.partial_mttkrp(xd, hs, side, plan).data, first), side
+
+
+def test_grid_empty_row_blocks_tolerated(P):
+    """test_driver.py:238-244: more slice members than factor rows for some of them."""
+    rng = np.random.default_rng(13)
+    hs = [rng.random((d, 2)) for d in (5, 3, 4)]
+    x = P.DenseTensor((5, 3, 4), O.reconstruct(hs, np.ones(2)))
+    seq = P.nncp_sequential(x, P.RunConfig(rank=2, algorithm="bpp", max_iters=3, tol=0.0, seed=6))
+    par = P.nncp_parallel(x, P.RunConfig(rank=2, algorithm="bpp", max_iters=3, tol=0.0, seed=6, grid=(1, 2, 4)))
+    assert np.allclose(seq.errors, par.errors, rtol=0, atol=1e-10)
+
+
+def test_grid_runs_bitwise_reproducible(P, golden):
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, "hals4", grid=(2, 2, 2, 1))
+    a = P.nncp_parallel(x, cfg)
+    b = P.nncp_parallel(x, cfg)
+    assert a.errors == b.errors
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("dims,r,algo,iters", [((128, 128, 128), 16, "hals", 8), ((32, 32, 32, 32), 32, "bpp", 4),
+                                               ((256, 128, 16), 20, "hals", 6), ((96, 80, 64), 64, "mu", 5),
+                                               ((160, 144, 120), 24, "bpp", 4)])
+def test_runs_vs_oracle_tma_sizes(P, dims, r, algo, iters):
+    """Full sequential runs on the TMA/split-K paths (BASELINE config shapes scaled down) vs the oracle."""
+    rng = np.random.default_rng(sum(dims) * r)
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    x = x + 0.01 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))
+    errors, factors, lam, _, _ = O.run_sequential(x, dims, r, algo, iters, 0.0, 0)
+    rep = P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0))
+    assert np.max(np.abs(np.array(rep.errors) - np.array(errors))) <= TRACE_TOL
+    for a, b in zip(rep.model.factors, factors):
+        assert np.max(np.abs(a - b)) <= FACTOR_TOL
