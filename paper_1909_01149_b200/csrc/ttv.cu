@@ -3,9 +3,11 @@
 // mode fastest (dimtree.py:68-99), so block r is the L x J matrix T_r.
 //   trailing: out[l, r] = sum_j T_r[l, j] * KRP(coeff)[j, r]   (dimtree.py:159-165)
 //   leading : out[j, r] = sum_l T_r[l, j] * H[l, r]             (dimtree.py:166-172)
-// Both are HBM-bound (one read of T, R flops per element); loads are coalesced
-// along the contiguous leading mode and reductions are fixed-order (warp shuffle
-// trees / ordered shared-memory sums), so results are run-to-run deterministic.
+// Both are HBM-bound (one read of T, one FMA per element).  The coefficient
+// column of a CTA's rank r is gathered once into shared memory (the factor rows
+// are R doubles apart, so reading them per element would cost 4x the sectors of
+// T itself), T is streamed with 16-byte loads along the contiguous leading mode,
+// and every reduction is fixed-order: run-to-run bitwise deterministic.
 #include "common.cuh"
 
 namespace nncp {
@@ -18,62 +20,119 @@ struct CoeffSpec {
 
 __device__ __forceinline__ double coeff_value(const CoeffSpec& s, int64_t j, int r, int R) {
   double v = 1.0;
-  for (int f = 0; f < s.n - 1; ++f) {
-    const int64_t d = s.dim[f];
-    const int64_t q = j / d;
-    v *= __ldg(s.ptr[f] + (j - q * d) * R + r);
-    j = q;
+#pragma unroll
+  for (int f = 0; f < kMaxOrder; ++f) {
+    if (f < s.n) {
+      int64_t row = j;
+      if (f != s.n - 1) {
+        const int64_t q = j / s.dim[f];
+        row = j - q * s.dim[f];
+        j = q;
+      }
+      v *= __ldg(s.ptr[f] + row * R + r);
+    }
   }
-  return v * __ldg(s.ptr[s.n - 1] + j * R + r);
+  return v;
 }
 
-// One CTA per (32 leading rows, rank r); 8 warps split the trailing index j.
+constexpr int kTtvChunk = 4096;  // coefficient entries staged per pass (32 KB)
+
+// trailing: CTA = (tile of 128 leading rows, rank r).  Lane pairs of rows are read
+// as double2 (when the leading extent is even); the 8 warps split the trailing
+// index, 4 loads in flight per lane; partial sums combined in warp order.
 __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restrict__ t, int64_t L, int64_t J,
-                                                           const CoeffSpec cs, int R, double* __restrict__ out) {
-  __shared__ double part[8][33];
+                                                           const CoeffSpec cs, int R, double* __restrict__ out,
+                                                           bool vec) {
+  __shared__ double coef[kTtvChunk];
+  __shared__ double2 part[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.y;
-  const int64_t l = int64_t(blockIdx.x) * 32 + lane;
+  const int64_t l0 = int64_t(blockIdx.x) * 128 + 2 * lane;  // this lane: rows l0, l0+1 (+64, +65)
   const double* tr = t + L * J * r;
-  double s0 = 0.0, s1 = 0.0;
-  int64_t j = warp;
-  if (l < L) {
-    for (; j + 8 < J; j += 16) {
-      const double c0 = coeff_value(cs, j, r, R);
-      const double c1 = coeff_value(cs, j + 8, r, R);
-      s0 = fma(__ldcs(tr + l + L * j), c0, s0);
-      s1 = fma(__ldcs(tr + l + L * (j + 8)), c1, s1);
-    }
-    if (j < J) s0 = fma(__ldcs(tr + l + L * j), coeff_value(cs, j, r, R), s0);
-  }
-  part[warp][lane] = s0 + s1;
-  __syncthreads();
-  if (warp == 0 && l < L) {
-    double s = part[0][lane];
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+  for (int64_t jc = 0; jc < J; jc += kTtvChunk) {
+    const int nj = int(min<int64_t>(kTtvChunk, J - jc));
+    __syncthreads();
+    for (int q = threadIdx.x; q < nj; q += blockDim.x) coef[q] = coeff_value(cs, jc + q, r, R);
+    __syncthreads();
+    for (int jj = warp; jj < nj; jj += 8) {
+      const double c = coef[jj];
+      const double* col = tr + L * (jc + jj);
 #pragma unroll
-    for (int w = 1; w < 8; ++w) s += part[w][lane];
-    out[l + L * r] = s;
+      for (int h = 0; h < 2; ++h) {
+        const int64_t l = l0 + 64 * h;
+        double2 v;
+        if (vec && l + 1 < L) {
+          v = __ldcs(reinterpret_cast<const double2*>(col + l));
+        } else {
+          v.x = (l < L) ? __ldcs(col + l) : 0.0;
+          v.y = (l + 1 < L) ? __ldcs(col + l + 1) : 0.0;
+        }
+        double2& a = h ? acc1 : acc0;
+        a.x = fma(v.x, c, a.x);
+        a.y = fma(v.y, c, a.y);
+      }
+    }
+  }
+  __syncthreads();
+  part[warp][lane] = acc0;
+  part[warp][lane + 32] = acc1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double2 s = part[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      s.x += part[w][threadIdx.x].x;
+      s.y += part[w][threadIdx.x].y;
+    }
+    const int64_t l = int64_t(blockIdx.x) * 128 + 2 * (threadIdx.x & 31) + 64 * (threadIdx.x >> 5);
+    if (l < L) out[l + L * r] = s.x;
+    if (l + 1 < L) out[l + 1 + L * r] = s.y;
   }
 }
 
-// One warp per (j, r): lanes stream the contiguous leading mode, shuffle reduce.
+// leading: CTA = (rank r, 64 consecutive trailing indices j); H[:, r] staged in
+// shared memory per pass of kTtvChunk leading rows; each warp owns 8 j columns.
 __global__ void __launch_bounds__(256) ttv_leading_kernel(const double* __restrict__ t, int64_t L, int64_t J,
                                                           const double* __restrict__ h, int R,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, bool vec) {
+  __shared__ double hc[kTtvChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j = int64_t(blockIdx.x) * 8 + warp;
   const int r = blockIdx.y;
-  if (j >= J) return;
-  const double* col = t + L * J * r + L * j;
-  double s0 = 0.0, s1 = 0.0;
-  int64_t l = lane;
-  for (; l + 32 < L; l += 64) {
-    s0 = fma(__ldcs(col + l), __ldg(h + l * R + r), s0);
-    s1 = fma(__ldcs(col + l + 32), __ldg(h + (l + 32) * R + r), s1);
+  const int64_t j0 = int64_t(blockIdx.x) * 64 + warp * 8;
+  const double* tr = t + L * J * r;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int64_t lc = 0; lc < L; lc += kTtvChunk) {
+    const int nl = int(min<int64_t>(kTtvChunk, L - lc));
+    __syncthreads();
+    for (int q = threadIdx.x; q < nl; q += blockDim.x) hc[q] = __ldg(h + (lc + q) * R + r);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = j0 + q;
+      if (j >= J) break;
+      const double* col = tr + L * j + lc;
+      double s = 0.0;
+      if (vec) {
+        for (int l = 2 * lane; l < nl; l += 64) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(col + l));
+          s = fma(v.x, hc[l], s);
+          s = fma(v.y, hc[l + 1], s);
+        }
+      } else {
+        for (int l = lane; l < nl; l += 32) s = fma(__ldcs(col + l), hc[l], s);
+      }
+      acc[q] += s;
+    }
   }
-  if (l < L) s0 = fma(__ldcs(col + l), __ldg(h + l * R + r), s0);
-  const double s = warp_sum(s0 + s1);
-  if (lane == 0) out[j + J * r] = s;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double s = warp_sum(acc[q]);
+    const int64_t j = j0 + q;
+    if (lane == 0 && j < J) out[j + J * r] = s;
+  }
 }
 
 __global__ void temp_to_rows_kernel(const double* __restrict__ t, int64_t rows, int R, double* __restrict__ out) {
@@ -91,6 +150,8 @@ int multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, i
   const int64_t L = ret_dims[0];
   int64_t J = 1;
   for (int n = 1; n < nret; ++n) J *= ret_dims[n];
+  // 16-byte loads need an even leading extent and an aligned base
+  const bool vec = (reinterpret_cast<uintptr_t>(temp) % 16) == 0 && (L % 2) == 0;
   if (side == NNCP_TTV_TRAILING) {
     if (ncoeff < 1 || ncoeff > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad coefficient count");
     CoeffSpec cs{};
@@ -102,12 +163,12 @@ int multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, i
       prod *= coeff_rows[f];
     }
     if (prod != J) return fail(NNCP_ERR_VALUE, "coeff rows do not match the trailing dimension");
-    dim3 grid(unsigned((L + 31) / 32), unsigned(rank));
-    ttv_trailing_kernel<<<grid, 256, 0, st>>>(temp, L, J, cs, rank, out);
+    dim3 grid(unsigned((L + 127) / 128), unsigned(rank));
+    ttv_trailing_kernel<<<grid, 256, 0, st>>>(temp, L, J, cs, rank, out, vec);
   } else if (side == NNCP_TTV_LEADING) {
     if (ncoeff != 1 || coeff_rows[0] != L) return fail(NNCP_ERR_VALUE, "coeff rows do not match the leading dimension");
-    dim3 grid(unsigned((J + 7) / 8), unsigned(rank));
-    ttv_leading_kernel<<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out);
+    dim3 grid(unsigned((J + 63) / 64), unsigned(rank));
+    ttv_leading_kernel<<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec);
   } else {
     return fail(NNCP_ERR_VALUE, "side must be trailing or leading");
   }
