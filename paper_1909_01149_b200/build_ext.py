@@ -39,6 +39,8 @@ def _compile(src: str) -> tuple[str, str]:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    if os.path.exists(OUT):
+        os.remove(OUT)  # a failed build must not leave a stale library behind
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(_compile, SOURCES))
     if verbose:

@@ -143,14 +143,18 @@ struct LeftTile {
   static constexpr int A_ELEMS = BM * BK;
   static constexpr int B_ELEMS = BK * RP;
   static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * 8 + 2 * STAGES * 8;
-  static_assert(size_t(RP) * BM * 8 <= size_t(STAGES) * A_ELEMS * 8, "epilogue tile must fit");
 };
 
+// Persistent: gridDim.x <= SM count CTAs loop over work items (row tile, K split)
+// in round-robin order; the producer/consumer ring runs continuously across items,
+// so a short contraction (c4: K = 256) does not pay a pipeline fill per tile.  The
+// epilogue stores straight from the accumulator registers (the smem ring is already
+// being refilled with the next item's stages).
 template <int RP, int NFM>
 __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
     mttkrp_left_tma(const __grid_constant__ CUtensorMap xmap, const KrpSpec krp, const int64_t M,
-                    const int64_t K, const int64_t k_per_split, double* __restrict__ out,
-                    const int64_t split_stride, const int R) {
+                    const int64_t K, const int64_t k_per_split, const int64_t tiles, const int64_t items,
+                    double* __restrict__ out, const int64_t split_stride, const int R) {
   using T = LeftTile<RP>;
   constexpr int BM = T::BM, BK = T::BK, NF = T::NF, ST = T::STAGES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -161,10 +165,6 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
-  const int64_t m0 = int64_t(blockIdx.x) * BM;
-  const int64_t kb = int64_t(blockIdx.y) * k_per_split;
-  const int64_t ke = min(K, kb + k_per_split);
-  const int nchunks = int((ke - kb + BK - 1) / BK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -181,81 +181,93 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
     // ---------------- producers: TMA for X, on-the-fly KRP rows for B ---------
     constexpr int UP = BK / 4 / T::PRODUCERS;
     static_assert(UP * T::PRODUCERS == BK / 4, "stage steps must split evenly");
-    KrpCursor<UP, NFM> cur;
-    cur.init(krp, [&](int t, int cc) { return kb + 4 * (t + pw * UP) + cc; }, lane & 3);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int s = ch % ST;
-      if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
-      const int64_t k0 = kb + int64_t(ch) * BK;
-      if (pw == 0 && lane == 0) {
-        // one arrival that also arms the transaction count, ordered before the copy
-        mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
-        tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(m0), int(k0));
+    uint32_t gch = 0;  // chunks produced by this CTA so far (ring position)
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      const int64_t m0 = (w % tiles) * BM;
+      const int64_t kb = (w / tiles) * k_per_split;
+      const int64_t ke = min(K, kb + k_per_split);
+      const int nchunks = int((ke - kb + BK - 1) / BK);
+      KrpCursor<UP, NFM> cur;
+      cur.init(krp, [&](int t, int cc) { return kb + 4 * (t + pw * UP) + cc; }, lane & 3);
+      for (int ch = 0; ch < nchunks; ++ch, ++gch) {
+        const int s = int(gch % ST);
+        if (gch >= uint32_t(ST)) mbar_wait(&empty[s], ((gch / ST) - 1) & 1);
+        const int64_t k0 = kb + int64_t(ch) * BK;
+        if (pw == 0 && lane == 0) {
+          // one arrival that also arms the transaction count, ordered before the copy
+          mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
+          tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(m0), int(k0));
+        }
+        produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, ke);
+        cur.advance(krp, BK);
+        mbar_arrive(&full[s]);
       }
-      produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, ke);
-      cur.advance(krp, BK);
-      mbar_arrive(&full[s]);
     }
     // producer tail: stay resident until the consumers released every stage
-    for (int ch = max(0, nchunks - ST); ch < nchunks; ++ch) mbar_wait(&empty[ch % ST], (ch / ST) & 1);
+    for (uint32_t q = gch > uint32_t(ST) ? gch - ST : 0; q < gch; ++q) mbar_wait(&empty[q % ST], (q / ST) & 1);
     return;
   }
 
   // ---------------- consumers: DMMA over the staged tiles ---------------------
-  double acc[4][NF][2];
+  uint32_t gch = 0;
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int64_t m0 = (w % tiles) * BM;
+    const int64_t kb = (w / tiles) * k_per_split;
+    const int64_t ke = min(K, kb + k_per_split);
+    const int nchunks = int((ke - kb + BK - 1) / BK);
+    double acc[4][NF][2];
 #pragma unroll
-  for (int f = 0; f < 4; ++f)
+    for (int f = 0; f < 4; ++f)
 #pragma unroll
-    for (int j = 0; j < NF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
+      for (int j = 0; j < NF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
 
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int s = ch % ST;
-    mbar_wait(&full[s], (ch / ST) & 1);
-    const double* as = As + s * T::A_ELEMS + warp * 32 + 2 * g;
-    const double* bs = Bs + s * T::B_ELEMS + lane;
+    for (int ch = 0; ch < nchunks; ++ch, ++gch) {
+      const int s = int(gch % ST);
+      mbar_wait(&full[s], (gch / ST) & 1);
+      const double* as = As + s * T::A_ELEMS + warp * 32 + 2 * g;
+      const double* bs = Bs + s * T::B_ELEMS + lane;
 #pragma unroll
-    for (int t = 0; t < BK / 4; ++t) {
-      double a[4], b[NF];
+      for (int t = 0; t < BK / 4; ++t) {
+        double a[4], b[NF];
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        // fragment rows: frag 2p row g <-> m = 16p + 2g, frag 2p+1 row g <-> m = 16p + 2g + 1
-        const double2 v = *reinterpret_cast<const double2*>(as + (4 * t + c) * BM + 16 * p);
-        a[2 * p] = v.x;
-        a[2 * p + 1] = v.y;
+        for (int p = 0; p < 2; ++p) {
+          // fragment rows: frag 2p row g <-> m = 16p + 2g, frag 2p+1 row g <-> m = 16p + 2g + 1
+          const double2 v = *reinterpret_cast<const double2*>(as + (4 * t + c) * BM + 16 * p);
+          a[2 * p] = v.x;
+          a[2 * p + 1] = v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < NF; ++j) b[j] = bs[(t * NF + j) * 32];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], a[f], b[j]);
       }
-#pragma unroll
-      for (int j = 0; j < NF; ++j) b[j] = bs[(t * NF + j) * 32];
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], a[f], b[j]);
+      // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
+      // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
+      // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
+      // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
-    // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
-    // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
-    // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
 
-  // ---------------- epilogue: registers -> smem [r][m] -> coalesced stores ----
-  named_bar_sync(1, 256);
-  double* Cs = As;
+    // ---------------- epilogue: accumulator registers -> HBM ------------------
+    // lanes of a store cover 8 rows (stride 2) x 4 columns; the (f, f^1) pair fills
+    // each 32-byte sector, merged in L2 before write-back.
+    double* o = out + (w / tiles) * split_stride;
 #pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    const int ml = warp * 32 + (f >> 1) * 16 + 2 * g + (f & 1);
+    for (int f = 0; f < 4; ++f) {
+      const int64_t m = m0 + warp * 32 + (f >> 1) * 16 + 2 * g + (f & 1);
+      if (m < M) {
 #pragma unroll
-    for (int j = 0; j < NF; ++j) {
-      Cs[(8 * j + 2 * c) * BM + ml] = acc[f][j][0];
-      Cs[(8 * j + 2 * c + 1) * BM + ml] = acc[f][j][1];
+        for (int j = 0; j < NF; ++j) {
+          const int r = 8 * j + 2 * c;
+          if (r < R) o[m + M * r] = acc[f][j][0];
+          if (r + 1 < R) o[m + M * (r + 1)] = acc[f][j][1];
+        }
+      }
     }
-  }
-  named_bar_sync(1, 256);
-  double* o = out + int64_t(blockIdx.y) * split_stride;
-  const int ml = threadIdx.x;
-  if (m0 + ml < M) {
-    for (int r = 0; r < R; ++r) o[m0 + ml + M * r] = Cs[r * BM + ml];
   }
 }
 
@@ -531,8 +543,10 @@ int launch_left_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan
                                        int(T::SMEM)));
     attr = true;
   }
-  dim3 grid(unsigned(p.tiles), unsigned(p.splits));
-  mttkrp_left_tma<RP, NFM><<<grid, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
+  const int64_t items = p.tiles * p.splits;
+  const unsigned ctas = unsigned(std::min<int64_t>(items, num_sms()));
+  mttkrp_left_tma<RP, NFM><<<ctas, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, p.tiles, items, dst,
+                                                              stride, R);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restr
   const double* tr = t + L * J * r;
   double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
   for (int64_t jc = 0; jc < J; jc += kTtvChunk) {
-    const int nj = int(min<int64_t>(kTtvChunk, J - jc));
+    const int nj = int(J - jc < kTtvChunk ? J - jc : int64_t(kTtvChunk));
     __syncthreads();
     for (int q = threadIdx.x; q < nj; q += blockDim.x) coef[q] = coeff_value(cs, jc + q, r, R);
     __syncthreads();
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) ttv_leading_kernel(const double* __restri
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.0;
   for (int64_t lc = 0; lc < L; lc += kTtvChunk) {
-    const int nl = int(min<int64_t>(kTtvChunk, L - lc));
+    const int nl = int(L - lc < kTtvChunk ? L - lc : int64_t(kTtvChunk));
     __syncthreads();
     for (int q = threadIdx.x; q < nl; q += blockDim.x) hc[q] = __ldg(h + (lc + q) * R + r);
     __syncthreads();
