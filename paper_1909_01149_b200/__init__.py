@@ -17,5 +17,7 @@ from .tensor_ops import (DenseTensor, FactorSet, gram, hadamard_grams_excluding,
 from .updaters import (BppCyclingError, UpdateInputs, UpdaterState, admm_update, bpp_update,  # noqa: F401
                        hals_update, mu_update, nesterov_update, ucp_update)
 from .synth import synthetic_tensor, truth_factors  # noqa: F401
+from .tensor_io import (SyntheticSpec, TensorFileError, generate_synthetic, read_matrix, read_tensor,  # noqa: F401
+                        write_matrix, write_tensor)
 
 __version__ = "0.1.0"

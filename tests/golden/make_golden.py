@@ -191,12 +191,27 @@ def init_cases():
     np.savez_compressed(os.path.join(OUT, "init.npz"), **out)
 
 
+def synthetic_cases():
+    """Reference generate_synthetic truth factors + tensor (tensor_io.py:103-125)."""
+    from nncp import SyntheticSpec, generate_synthetic
+
+    spec = SyntheticSpec((9, 8, 7), 3, seed=13)
+    x, truth = generate_synthetic(spec)
+    out = {"dims": np.array(spec.dims), "rank": np.array(spec.rank), "seed": np.array(spec.seed), "x": x.data}
+    for n, h in enumerate(truth.factors):
+        out[f"h{n}"] = h
+    np.savez_compressed(os.path.join(OUT, "synthetic.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference nncp", nncp.__version__, "numpy", np.__version__)
     mttkrp_cases()
     update_cases()
     run_cases()
     init_cases()
+    synthetic_cases()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
