@@ -51,6 +51,7 @@ extern "C" {
 #define NNCP_ALGO_MU 1        /* updaters.py:91-94   */
 #define NNCP_ALGO_HALS 2      /* updaters.py:97-118  */
 #define NNCP_ALGO_BPP 3       /* updaters.py:121-164 */
+#define NNCP_ALGO_UCP 4       /* updaters.py:77-88 (status[0] bit 0: ridge applied; status[3] = 3: still singular) */
 
 /* status words (device int32[NNCP_STATUS_WORDS]) written by nncp_update:
  *   [0],[1]  HALS: bit r set when gram diagonal r <= 0 (updaters.py:110-113)
@@ -112,7 +113,7 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank,
                 void* stream);
 
 /* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
- * gram = owned^T owned (raw, local rows).  owned may alias hhat. */
+ * gram = owned^T owned (raw, local rows).  owned may alias hhat; lam and gram may be NULL. */
 int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank,
                         double* owned, double* lam, double* gram, void* ws, size_t ws_bytes,
                         void* stream);
@@ -128,6 +129,36 @@ int nncp_gamma(const double* grams, int order, int rank, const double* lam, doub
 /* tensor_ops.py:208-212 matrix_inner_product <a, b * lam> (lam may be NULL). */
 int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank,
                double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- the remaining update rules -------------------------- */
+
+/* One ADMM inner step for all rows (updaters.py:196-215): xhat = (S + rho I)^-1 (m + rho (x + u)),
+ * x_out = max(xhat - u, 0), u += x_out - xhat (in place); sums5 = local [|x-xhat|^2, |x|^2,
+ * |xhat|^2, |x-xprev|^2, |u|^2] for the hook, sums5[5] = the rho used (6 doubles).
+ * rho <= 0: tr(S)/R (updaters.py:167-170).
+ * S as in nncp_update (Grams + mode, or order == 0 and S given). */
+int nncp_admm_step(const double* grams, int order, int mode, int rank, double rho, const double* mttkrp_rows,
+                   const double* x_in, double* u, double* x_out, int64_t rows, double* sums5, int* status,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* nesterov_hyperparams (updaters.py:223-243): hyper3 = (lam, alpha, beta) from the extreme
+ * eigenvalues of S (device Jacobi). */
+int nncp_nes_hyper(const double* grams, int order, int mode, int rank, double prox_floor, double* hyper3,
+                   void* stream);
+
+/* One accelerated projected-gradient step (updaters.py:266-277) for all rows; maxes2 = local
+ * [max |x_out - x_in|, max |x_out|] for the max-hook. */
+int nncp_nes_step(const double* grams, int order, int mode, int rank, const double* hyper3,
+                  const double* mttkrp_rows, const double* y_in, const double* x_in, const double* xstar,
+                  double* x_out, double* y_out, int64_t rows, double* maxes2, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* Elementwise helpers of the driver (driver.py:403, 464-486). */
+int nncp_scale_columns(const double* in, const double* colscale, int64_t rows, int rank, double* out,
+                       void* stream);
+int nncp_extrapolate(const double* cur, const double* prev, int64_t n, double step, double* out, void* stream);
+int nncp_nes_lambda(const double* cand_lam, const double* nsq, int order, int rank, double* lam, void* stream);
+int nncp_colsumsq(const double* h, int64_t rows, int rank, double* nsq, void* ws, size_t ws_bytes, void* stream);
 
 /* Synthetic input (BASELINE.json configs; tensor_io.py:103-125 generalised with noise):
  * x[i] = sum_r prod_n H_n(i_n, r) + noise_scale * |N(0,1)|_i, the Gaussian drawn from

@@ -21,7 +21,7 @@ NNCP_ERR_CUDA = 3
 NNCP_ERR_UNSUPPORTED = 4
 SIDE_LEFT, SIDE_RIGHT = 0, 1
 TTV_TRAILING, TTV_LEADING = 0, 1
-ALGO_CODES = {"mu": 1, "hals": 2, "bpp": 3}
+ALGO_CODES = {"mu": 1, "hals": 2, "bpp": 3, "ucp": 4}
 MAX_ORDER = 8
 MAX_RANK = 64
 STATUS_WORDS = 4
@@ -54,6 +54,17 @@ SIGNATURES = [
     ("nncp_gram", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gamma", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
     ("nncp_inner", ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
+    ("nncp_admm_step", ctypes.c_int,
+     [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, vp, vp, vp, vp, ctypes.c_int64,
+      vp, vp, vp, ctypes.c_size_t, vp]),
+    ("nncp_nes_hyper", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, vp, vp]),
+    ("nncp_nes_step", ctypes.c_int,
+     [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp,
+      ctypes.c_size_t, vp]),
+    ("nncp_scale_columns", ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp]),
+    ("nncp_extrapolate", ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp]),
+    ("nncp_nes_lambda", ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+    ("nncp_colsumsq", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_synthetic", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, c_i64p, c_i64p, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_double,
       ctypes.c_uint64, vp]),

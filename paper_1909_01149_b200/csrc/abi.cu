@@ -35,6 +35,17 @@ int inner(const double*, const double*, const double*, int64_t, int, double*, vo
 int norm_squared(const double*, int64_t, double*, void*, size_t, cudaStream_t);
 int status_reset(int*, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
+int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
+        cudaStream_t);
+int admm_step(const double*, int, int, int, double, const double*, const double*, double*, double*, int64_t, double*,
+              int*, void*, size_t, cudaStream_t);
+int nes_hyper(const double*, int, int, int, double, double*, cudaStream_t);
+int nes_step(const double*, int, int, int, const double*, const double*, const double*, const double*, const double*,
+             double*, double*, int64_t, double*, void*, size_t, cudaStream_t);
+int scale_columns(const double*, const double*, int64_t, int, double*, cudaStream_t);
+int extrapolate(const double*, const double*, int64_t, double, double*, cudaStream_t);
+int nes_lambda(const double*, const double*, int, int, double*, cudaStream_t);
+int colsumsq(const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int synthetic(double*, int, const int64_t*, const int64_t*, const int64_t*, const double* const*, int, double,
               uint64_t, cudaStream_t);
 
@@ -123,6 +134,14 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank, co
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
   if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
   if (!status) return fail(NNCP_ERR_VALUE, "status buffer required");
+  if (algo == NNCP_ALGO_UCP) {
+    if (rows <= 0) {
+      if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, S(stream)));
+      if (beta) NNCP_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), S(stream)));
+      return NNCP_OK;
+    }
+    return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream));
+  }
   return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
                 S(stream));
 }
@@ -147,6 +166,56 @@ int nncp_gamma(const double* grams, int order, int rank, const double* lam, doub
 int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank, double* out, void* ws,
                size_t ws_bytes, void* stream) {
   return inner(a, b, lam, rows, rank, out, ws, ws_bytes, S(stream));
+}
+
+static int check_rank_mode(int order, int mode, int rank) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
+  if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
+  if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
+  return NNCP_OK;
+}
+
+int nncp_admm_step(const double* grams, int order, int mode, int rank, double rho, const double* mttkrp_rows,
+                   const double* x_in, double* u, double* x_out, int64_t rows, double* sums5, int* status, void* ws,
+                   size_t ws_bytes, void* stream) {
+  int rc = check_rank_mode(order, mode, rank);
+  if (rc) return rc;
+  return admm_step(grams, order, mode, rank, rho, mttkrp_rows, x_in, u, x_out, std::max<int64_t>(rows, 0), sums5,
+                   status, ws, ws_bytes, S(stream));
+}
+
+int nncp_nes_hyper(const double* grams, int order, int mode, int rank, double prox_floor, double* hyper3,
+                   void* stream) {
+  int rc = check_rank_mode(order, mode, rank);
+  if (rc) return rc;
+  return nes_hyper(grams, order, mode, rank, prox_floor, hyper3, S(stream));
+}
+
+int nncp_nes_step(const double* grams, int order, int mode, int rank, const double* hyper3, const double* mttkrp_rows,
+                  const double* y_in, const double* x_in, const double* xstar, double* x_out, double* y_out,
+                  int64_t rows, double* maxes2, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_rank_mode(order, mode, rank);
+  if (rc) return rc;
+  return nes_step(grams, order, mode, rank, hyper3, mttkrp_rows, y_in, x_in, xstar, x_out, y_out,
+                  std::max<int64_t>(rows, 0), maxes2, ws, ws_bytes, S(stream));
+}
+
+int nncp_scale_columns(const double* in, const double* colscale, int64_t rows, int rank, double* out, void* stream) {
+  return scale_columns(in, colscale, rows, rank, out, S(stream));
+}
+
+int nncp_extrapolate(const double* cur, const double* prev, int64_t n, double step, double* out, void* stream) {
+  return extrapolate(cur, prev, n, step, out, S(stream));
+}
+
+int nncp_nes_lambda(const double* cand_lam, const double* nsq, int order, int rank, double* lam, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  return nes_lambda(cand_lam, nsq, order, rank, lam, S(stream));
+}
+
+int nncp_colsumsq(const double* h, int64_t rows, int rank, double* nsq, void* ws, size_t ws_bytes, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  return colsumsq(h, std::max<int64_t>(rows, 0), rank, nsq, ws, ws_bytes, S(stream));
 }
 
 int nncp_synthetic(double* x, int order, const int64_t* local_dims, const int64_t* offsets,

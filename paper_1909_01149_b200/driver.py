@@ -33,14 +33,16 @@ from .dimtree import DimTreeContext, DimTreePlan
 from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, RankLayout, ThreadCollectives,
                    ThreadGrid, block_partition)
 from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
-from .updaters import BppCyclingError, raise_for_status  # noqa: F401  (re-exported semantics)
+from .updaters import (AdmmRunner, BppCyclingError, NesterovRunner, _SPack,  # noqa: F401
+                       raise_for_status)
 
 __all__ = ["ALGORITHMS", "CATEGORIES", "RunConfig", "RunReport", "init_factor", "nncp_parallel",
            "nncp_sequential", "record_category", "relative_error", "IN_SCOPE_ALGORITHMS", "run_local"]
 
 CATEGORIES = ("MTTKRP", "KRP", "MultiTTV", "Gram", "NNLS", "ReduceScatter", "AllGather", "AllReduce", "Error")
 ALGORITHMS = ("ucp", "mu", "hals", "bpp", "admm", "nes")
-IN_SCOPE_ALGORITHMS = ("mu", "hals", "bpp")
+IN_SCOPE_ALGORITHMS = ALGORITHMS          # all six update rules run on the device
+FUSED_ALGORITHMS = ("mu", "hals", "bpp", "ucp")   # one kernel per mode (CUDA-graph capturable)
 
 
 @dataclass
@@ -205,7 +207,7 @@ class _Engine:
         self.layout = layout
         self.N = len(self.dims)
         self.R = int(cfg.rank)
-        self.algo = _lib.ALGO_CODES[cfg.algorithm]
+        self.algo = _lib.ALGO_CODES.get(cfg.algorithm, 0)
         dev = x_local.device
         self.dev = dev
         if layout is None:
@@ -238,6 +240,16 @@ class _Engine:
         self.host_status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32).pin_memory()
         self.timer = _EventTimer(timing)
         self.lib = _lib.load()
+        # stateful rules (updaters.py:56-68): per-mode ADMM dual / Nesterov centre
+        rows_max = max(max(self.n_owned), 1)
+        if cfg.algorithm in ("admm", "nes"):
+            self.cur = torch.empty((rows_max, R), **f64)
+            if cfg.algorithm == "admm":
+                self.runner = AdmmRunner(rows_max, R, dev, self.ws)
+                self.admm_dual = [torch.zeros((self.n_owned[n], R), **f64) for n in range(N)]
+            else:
+                self.runner = NesterovRunner(rows_max, R, dev, self.ws)
+                self.nes_prev = [None] * N
         self.graph = None
         self.graph_kernels = 0      # library kernels captured in the sweep graph
         self.graph_replays = 0
@@ -331,11 +343,14 @@ class _Engine:
             m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
             self.timer.mark("ReduceScatter")
             last = n == N - 1
-            _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
-                                       _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
-                                       _lib.ptr(self.hhat), _lib.ptr(self.nsq),
-                                       _lib.ptr(self.scal) if last else None, _lib.ptr(self.status[n]),
-                                       self.ws.ptr, self.ws.nbytes, st))
+            if cfg.algorithm in FUSED_ALGORITHMS:
+                _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
+                                           _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
+                                           _lib.ptr(self.hhat), _lib.ptr(self.nsq),
+                                           _lib.ptr(self.scal) if last else None, _lib.ptr(self.status[n]),
+                                           self.ws.ptr, self.ws.nbytes, st))
+            else:
+                self._iterative_update(n, m_owned, last)
             self.timer.mark("NNLS")
             self.coll.all_reduce(self.nsq)
             self.timer.mark("AllReduce")
@@ -355,12 +370,103 @@ class _Engine:
         self.host_status.copy_(self.status, non_blocking=True)
         self.timer.mark("Error")
 
+    def _hook(self, t, op):
+        return self.coll.all_reduce(t, op)
+
+    def _iterative_update(self, n, m_owned, last):
+        """ADMM / NES for mode n (updaters.py:173-281) through the collective hook."""
+        lib, st, R = self.lib, self._st(), self.R
+        rows = self.n_owned[n]
+        cur = self.cur[:rows]
+        _lib.check(lib.nncp_scale_columns(_lib.ptr(self.owned[n]), _lib.ptr(self.lam), rows, R, _lib.ptr(cur), st))
+        spack = _SPack(self.grams, self.N, n)
+        try:
+            if self.cfg.algorithm == "admm":
+                x, _ = self.runner.run(spack, m_owned, cur, self.admm_dual[n], self._hook, status=self.status[n])
+            else:
+                xstar = self.nes_prev[n] if self.nes_prev[n] is not None else cur
+                x, _ = self.runner.run(spack, m_owned, cur, xstar, self._hook)
+                if self.nes_prev[n] is None:
+                    self.nes_prev[n] = torch.empty_like(x[:rows])
+                self.nes_prev[n].copy_(x[:rows])
+        except Exception as exc:
+            raise RuntimeError(f"NNLS update failed at iteration {len(self.report.errors)}, mode {n + 1}") from exc
+        hh = self.hhat[:rows]
+        hh.copy_(x[:rows])
+        _lib.check(lib.nncp_colsumsq(_lib.ptr(hh), rows, R, _lib.ptr(self.nsq), self.ws.ptr, self.ws.nbytes, st))
+        if last:
+            _lib.check(lib.nncp_inner(_lib.ptr(m_owned), _lib.ptr(hh), None, rows, R, _lib.ptr(self.scal),
+                                      self.ws.ptr, self.ws.nbytes, st))
+
+    # -- Nesterov outer extrapolation (driver.py:452-492) ----------------------------
+    def _snapshot(self):
+        self.prev_owned = [h.clone() for h in self.owned]
+        self.prev_shared = [h.clone() for h in self.shared] if self.coll.parallel else self.prev_owned
+        self.prev_lam = self.lam.clone()
+
+    def _model_error(self, cand_shared, cand_owned, cand_lam):
+        """driver.py:310-328 on device buffers."""
+        lib, st, R, N = self.lib, self._st(), self.R, self.N
+        mb = self.mbar[: self.dims[-1]]
+        if self.cfg.use_dimtree:
+            self.ctx.mttkrp_last_mode(self.x, cand_shared, out=mb)        # counts a tree partial, as the reference
+        else:
+            calls = self.ctx.partial_calls
+            self.ctx.mttkrp_direct(self.x, cand_shared, N - 1, out=mb)
+            self.ctx.partial_calls = calls
+        sc = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        _lib.check(lib.nncp_inner(_lib.ptr(mb), _lib.ptr(cand_shared[-1]), _lib.ptr(cand_lam), self.dims[-1], R,
+                                  _lib.ptr(sc), self.ws.ptr, self.ws.nbytes, st))
+        self.coll.all_reduce(sc[0:1])
+        grams = torch.zeros((N, R, R), dtype=torch.float64, device=self.dev)
+        for n in range(N):
+            _lib.check(lib.nncp_gram(_lib.ptr(cand_owned[n]), self.n_owned[n], R, _lib.ptr(grams[n]), self.ws.ptr,
+                                     self.ws.nbytes, st))
+            self.coll.all_reduce(grams[n])
+        _lib.check(lib.nncp_gamma(_lib.ptr(grams), N, R, _lib.ptr(cand_lam), _lib.vp(sc.data_ptr() + 8), st))
+        beta, gamma = sc.cpu().tolist()
+        return _eps_from_terms(self.alpha, beta, gamma)
+
+    def _nes_accelerate(self, it, eps):
+        lib, st, R, N = self.lib, self._st(), self.R, self.N
+        step = float(it) ** (1.0 / N)
+
+        def extrap(cur, prev):
+            out = torch.empty_like(cur)
+            _lib.check(lib.nncp_extrapolate(_lib.ptr(cur), _lib.ptr(prev), cur.numel(), step, _lib.ptr(out), st))
+            return out
+
+        cand_owned = [extrap(h, hp) for h, hp in zip(self.owned, self.prev_owned)]
+        cand_shared = ([extrap(h, hp) for h, hp in zip(self.shared, self.prev_shared)] if self.coll.parallel
+                       else cand_owned)
+        cand_lam = extrap(self.lam, self.prev_lam)
+        cand_eps = self._model_error(cand_shared, cand_owned, cand_lam)
+        if not cand_eps < eps:
+            return
+        nsq = torch.zeros((N, R), dtype=torch.float64, device=self.dev)
+        for n in range(N):
+            _lib.check(lib.nncp_colsumsq(_lib.ptr(cand_owned[n]), self.n_owned[n], R, _lib.ptr(nsq[n]), self.ws.ptr,
+                                         self.ws.nbytes, st))
+        self.coll.all_reduce(nsq)
+        for n in range(N):
+            _lib.check(lib.nncp_normalize_gram(_lib.ptr(cand_owned[n]), _lib.ptr(nsq[n]), self.n_owned[n], R,
+                                               _lib.ptr(self.owned[n]), None, None, self.ws.ptr, self.ws.nbytes, st))
+            if self.coll.parallel:
+                _lib.check(lib.nncp_normalize_gram(_lib.ptr(cand_shared[n]), _lib.ptr(nsq[n]), self.dims[n], R,
+                                                   _lib.ptr(self.shared[n]), None, None, self.ws.ptr,
+                                                   self.ws.nbytes, st))
+        _lib.check(lib.nncp_nes_lambda(_lib.ptr(cand_lam), _lib.ptr(nsq), N, R, _lib.ptr(self.lam), st))
+        for n in range(N):
+            _lib.check(lib.nncp_gram(_lib.ptr(self.owned[n]), self.n_owned[n], R, _lib.ptr(self.grams[n]),
+                                     self.ws.ptr, self.ws.nbytes, st))
+            self.coll.all_reduce(self.grams[n])
+
     def _finish_iteration(self, it):
         torch.cuda.current_stream().synchronize()
         status = self.host_status.tolist()
         for n in range(self.N):
             try:
-                raise_for_status(status[n], warn_hals=(self.cfg.algorithm == "hals"))
+                raise_for_status(status[n], self.cfg.algorithm)
             except Exception as exc:
                 raise RuntimeError(f"NNLS update failed at iteration {it}, mode {n + 1}") from exc
         beta, gamma = self.host_scal.tolist()
@@ -370,7 +476,7 @@ class _Engine:
         """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
         cfg = self.cfg
         errors = self.report.errors
-        use_graph = cfg.cuda_graph and not self.coll.parallel
+        use_graph = cfg.cuda_graph and not self.coll.parallel and cfg.algorithm in FUSED_ALGORITHMS
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
         for it in range(done + 1, stop + 1):
@@ -385,10 +491,14 @@ class _Engine:
                     self.ctx.partial_calls += 2
             else:
                 self.timer.start()
+                if cfg.algorithm == "nes":
+                    self._snapshot()
                 self._sweep()
             eps = self._finish_iteration(it)
             self.timer.collect(self.report.rows[-1])
             errors.append(eps)
+            if cfg.algorithm == "nes":
+                self._nes_accelerate(it, eps)
             self.report.row_wall[-1] = time.perf_counter() - wall0
             self.report.row_words[-1] = self.coll.counters.total_words() - sum(self.report.row_words[:-1])
             if eps <= cfg.tol:

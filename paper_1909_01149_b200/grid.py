@@ -185,6 +185,8 @@ class IdentityCollectives:
         self.counters = CommCounters()
 
     def all_reduce(self, t, op="sum"):
+        if op not in ("sum", "max", "min"):
+            raise ValueError(f"unknown reduction {op!r}")
         return t
 
     def reduce_scatter(self, mode, t, parts=None):
@@ -215,9 +217,10 @@ class DistCollectives:
         self.slice_pg = [dist_groups[n][c] for n, c in enumerate(layout.coord)]
 
     def all_reduce(self, t, op="sum"):
-        if op != "sum":
-            raise ValueError(f"only sum reductions are on this path, got {op!r}")
-        self.dist.all_reduce(t)
+        ops = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}
+        if op not in ops:
+            raise ValueError(f"unknown reduction {op!r}")
+        self.dist.all_reduce(t, op=ops[op])
         self.counters.record("AllReduce", t.numel(), t.numel())
         return t
 
@@ -324,14 +327,19 @@ class ThreadCollectives:
         torch.cuda.current_stream().synchronize()
 
     def all_reduce(self, t, op="sum"):
-        if op != "sum":
-            raise ValueError(f"only sum reductions are on this path, got {op!r}")
+        if op not in ("sum", "max", "min"):
+            raise ValueError(f"unknown reduction {op!r}")
         self._sync()
 
         def combine(slots):
             out = slots[0].clone()
-            for s in slots[1:]:
-                out += s
+            for s in slots[1:]:  # ascending rank order (grid.py:250-262)
+                if op == "sum":
+                    out += s
+                elif op == "max":
+                    torch.maximum(out, s, out=out)
+                else:
+                    torch.minimum(out, s, out=out)
             self._sync()
             return out
 

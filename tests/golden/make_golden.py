@@ -191,6 +191,67 @@ def init_cases():
     np.savez_compressed(os.path.join(OUT, "init.npz"), **out)
 
 
+def stateful_cases():
+    """UCP / ADMM / NES (updaters.py:77-88,167-281) on the update inputs + full runs."""
+    from nncp import UpdaterState, admm_update, nesterov_update, ucp_update
+    from nncp.updaters import nesterov_hyperparams
+
+    rng = np.random.default_rng(91)
+    out = {}
+    k = 0
+    for r in (1, 2, 3, 5, 8, 16, 20, 32):
+        for rows in (1, 9, 40):
+            a = rng.random((r + 6, r))
+            b = rng.random((r + 6, rows))
+            s = a.T @ a
+            s = 0.5 * (s + s.T)
+            m = b.T @ a
+            if k % 2 == 1:
+                m = m - 0.5 * np.abs(m).mean()
+            cur = rng.random((rows, r)) + 1e-3
+            out[f"s{k}_s"], out[f"s{k}_m"], out[f"s{k}_cur"] = s, m, cur
+            out[f"s{k}_ucp"] = ucp_update(UpdateInputs(s, m, cur))
+            st = UpdaterState()
+            out[f"s{k}_admm1"] = admm_update(UpdateInputs(s, m, cur), st)
+            out[f"s{k}_admm1_iters"] = np.array(st.last_inner_iters)
+            out[f"s{k}_admm2"] = admm_update(UpdateInputs(s, m, out[f"s{k}_admm1"]), st)
+            out[f"s{k}_admm_dual"] = st.admm_dual
+            nst = UpdaterState()
+            out[f"s{k}_nes"] = nesterov_update(UpdateInputs(s, m, cur), nst)
+            out[f"s{k}_nes_iters"] = np.array(nst.last_inner_iters)
+            out[f"s{k}_hyper"] = np.array(nesterov_hyperparams(s))
+            k += 1
+    out["nst"] = np.array(k)
+    # runs
+    cases = [("ucp3", (12, 10, 8), 3, "ucp", 6, 21), ("admm3", (14, 12, 10), 4, "admm", 8, 22),
+             ("nes3", (12, 11, 10), 3, "nes", 8, 23), ("admm4", (7, 6, 5, 4), 3, "admm", 6, 24),
+             ("nes4", (7, 6, 5, 4), 2, "nes", 6, 25), ("nes_r16", (24, 20, 18), 16, "nes", 5, 26)]
+    for name, dims, r, algo, iters, dseed in cases:
+        rng2 = np.random.default_rng(dseed)
+        data = noisy_lowrank(rng2, dims, r, 0.02)
+        x = DenseTensor(dims, data)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            rep = nncp_sequential(x, RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=1))
+        out[f"{name}_dims"] = np.array(dims)
+        out[f"{name}_meta"] = np.array([r, iters, 1])
+        out[f"{name}_algo"] = np.array(algo)
+        out[f"{name}_x"] = data
+        out[f"{name}_errors"] = np.array(rep.errors)
+        out[f"{name}_lam"] = rep.model.lam
+        out[f"{name}_partials"] = np.array(rep.tree_partial_calls)
+        for n, h in enumerate(rep.model.factors):
+            out[f"{name}_f{n}"] = h
+        if name in ("admm3", "nes3"):
+            par = nncp_parallel(x, RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=1,
+                                             grid=(2, 2, 1)))
+            out[f"{name}_grid_errors"] = np.array(par.errors)
+            out[f"{name}_grid_calls"] = np.array([par.counters.calls.get(c, 0) for c in
+                                                  ("ReduceScatter", "AllGather", "AllReduce")])
+    out["runs"] = np.array([c[0] for c in cases])
+    np.savez_compressed(os.path.join(OUT, "stateful.npz"), **out)
+
+
 def synthetic_cases():
     """Reference generate_synthetic truth factors + tensor (tensor_io.py:103-125)."""
     from nncp import SyntheticSpec, generate_synthetic
@@ -210,6 +271,7 @@ if __name__ == "__main__":
     run_cases()
     init_cases()
     synthetic_cases()
+    stateful_cases()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
