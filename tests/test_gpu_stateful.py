@@ -118,3 +118,17 @@ def test_runs_vs_golden(P, golden):
             assert np.max(np.abs(np.array(par.errors) - g[f"{name}_grid_errors"])) <= trace_tol, name
             calls = [par.counters.calls.get(c, 0) for c in ("ReduceScatter", "AllGather", "AllReduce")]
             assert calls == list(g[f"{name}_grid_calls"]), (name, calls)
+
+
+@pytest.mark.parametrize("algo", ["ucp", "mu", "hals", "bpp", "admm", "nes"])
+def test_uneven_dims_and_blocks_all_algorithms(P, algo):
+    """test_driver.py:227-236: sequential == (2,2,1) grid for every update rule."""
+    x, _ = P.generate_synthetic(P.SyntheticSpec((7, 5, 6), 2, seed=12))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        seq = P.nncp_sequential(x, P.RunConfig(rank=2, algorithm=algo, max_iters=6, tol=0.0, seed=5))
+        par = P.nncp_parallel(x, P.RunConfig(rank=2, algorithm=algo, max_iters=6, tol=0.0, seed=5, grid=(2, 2, 1)))
+    tol = 5e-8 if algo == "nes" else 1e-10
+    assert np.allclose(seq.errors, par.errors, rtol=0, atol=tol)
+    for a, b in zip(seq.model.factors, par.model.factors):
+        assert np.allclose(a, b, rtol=0, atol=max(tol, 1e-10) * 100)
