@@ -131,6 +131,21 @@ __device__ __forceinline__ void produce_krp(const KrpSpec& krp, const KrpCursor<
 // not fit the ~7 KB of L1 left next to the pipeline), so stages are split
 // across warps until the consumers, not the producers, set the pace.
 
+// Deferred stage release.  A consumer warp frees the stage it read in the previous
+// chunk only after the next chunk's full barrier fired: by then every DMMA of that
+// chunk has issued (the loop back-edge and the wait keep ptxas from hoisting the
+// arrive above them), so all of its ld.shared results have landed and the TMA
+// refill cannot overwrite data still being read.  (An arrive placed right after
+// the last k-step raced its in-flight loads: tools/debug_left.py.)  The final
+// release of a CTA goes through a proxy fence instead.
+__device__ __forceinline__ void release_stage(uint64_t* empty, int& pending, int lane) {
+  if (pending >= 0) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[pending]);
+    pending = -1;
+  }
+}
+
 // ------------------------------------------------------------ left side ----
 template <int RP>
 struct LeftTile {
@@ -210,6 +225,7 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
 
   // ---------------- consumers: DMMA over the staged tiles ---------------------
   uint32_t gch = 0;
+  int pending = -1;  // stage read in the previous chunk, released once the next one is ready
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
     const int64_t m0 = (w % tiles) * BM;
     const int64_t kb = (w / tiles) * k_per_split;
@@ -224,6 +240,7 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
     for (int ch = 0; ch < nchunks; ++ch, ++gch) {
       const int s = int(gch % ST);
       mbar_wait(&full[s], (gch / ST) & 1);
+      release_stage(empty, pending, lane);
       const double* as = As + s * T::A_ELEMS + warp * 32 + 2 * g;
       const double* bs = Bs + s * T::B_ELEMS + lane;
 #pragma unroll
@@ -243,13 +260,7 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], a[f], b[j]);
       }
-      // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
-      // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
-      // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
-      // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      pending = s;
     }
 
     // ---------------- epilogue: accumulator registers -> HBM ------------------
@@ -269,6 +280,8 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
       }
     }
   }
+  fence_proxy_async();
+  release_stage(empty, pending, lane);
 }
 
 // ------------------------------------------------------------ right side ---
@@ -351,9 +364,11 @@ __global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < NF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
 
+  int pending = -1;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int s = ch % ST;
     mbar_wait(&full[s], (ch / ST) & 1);
+    release_stage(empty, pending, lane);
     const double* as = As + s * T::A_ELEMS + (warp * 32 + g) * BMC + 2 * c;
     const double* bs = Bs + s * T::B_ELEMS + lane;
 #pragma unroll
@@ -378,14 +393,10 @@ __global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
           dmma884(acc[f][j][0], acc[f][j][1], ahi[f], bhi[j]);
         }
     }
-    // The stage is about to be refilled by TMA (async proxy).  An mbarrier arrive
-    // does not wait for this warp's in-flight ld.shared, and ptxas hoists it above
-    // the trailing DMMAs; the proxy fence drains the generic-proxy reads first
-    // (without it the refill raced the last k-step's loads -- tools/debug_left.py).
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    pending = s;
   }
+  fence_proxy_async();
+  release_stage(empty, pending, lane);
 
   named_bar_sync(1, 256);
   double* Cs = As;
