@@ -319,22 +319,26 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------- scalars -----
-__global__ void gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
-                             double* __restrict__ gamma) {
+__global__ void __launch_bounds__(256)
+    gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
+                 double* __restrict__ gamma) {
+  __shared__ double W[kMaxRank * kMaxRank];
   __shared__ double v[kMaxRank];
-  const int a = threadIdx.x;
-  if (a < R) {
-    double s = 0.0;
-    for (int b = 0; b < R; ++b) {
-      double p = 1.0;
-      for (int m = 0; m < order; ++m) {
-        const double* g = grams + size_t(m) * R * R;
-        const double sym = 0.5 * (g[a * R + b] + g[b * R + a]);
-        p = (m == 0) ? sym : p * sym;
-      }
-      s = fma(p, lam[b], s);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    double p = 1.0;
+    for (int m = 0; m < order; ++m) {
+      const double* g = grams + size_t(m) * R * R;
+      const double sym = 0.5 * (g[a * R + b] + g[b * R + a]);
+      p = (m == 0) ? sym : p * sym;
     }
-    v[a] = s;
+    W[e] = p * lam[b];
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int b = 0; b < R; ++b) s += W[threadIdx.x * R + b];
+    v[threadIdx.x] = s;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -357,13 +361,7 @@ __global__ void __launch_bounds__(256)
   }
   s = block_sum(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
-  if (last_cta_ticket(ticket)) {
-    if (threadIdx.x == 0) {
-      double t = part[0];
-      for (unsigned k = 1; k < gridDim.x; ++k) t += part[k];
-      out[0] = t;
-    }
-  }
+  if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, 1, out);
 }
 
 __global__ void __launch_bounds__(512)
@@ -381,13 +379,7 @@ __global__ void __launch_bounds__(512)
   if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s0 = fma(x[n - 1], x[n - 1], s0);
   const double s = block_sum(s0 + s1, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
-  if (last_cta_ticket(ticket)) {
-    if (threadIdx.x == 0) {
-      double t = part[0];
-      for (unsigned k = 1; k < gridDim.x; ++k) t += part[k];
-      out[0] = t;
-    }
-  }
+  if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, 1, out);
 }
 
 __global__ void status_reset_kernel(int* status) {
@@ -481,7 +473,7 @@ int normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank
 }
 
 int gamma(const double* grams, int order, int rank, const double* lam, double* out, cudaStream_t st) {
-  gamma_kernel<<<1, 64, 0, st>>>(grams, order, rank, lam, out);
+  gamma_kernel<<<1, 256, 0, st>>>(grams, order, rank, lam, out);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

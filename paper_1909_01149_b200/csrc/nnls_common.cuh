@@ -39,12 +39,50 @@ static __device__ double block_sum(double v, double* red) {
   return s;
 }
 
-// Final fixed-order reduction of per-CTA partials [nblk][n] -> out[n] by the last CTA.
+// Final fixed-order reduction of per-CTA partials [nblk][n] -> out[n], run by the
+// last CTA.  Latency-bound if done naively (one thread walking nblk partials), so
+// each output is split into `segs` strided segments with four independent
+// accumulators, then the segments are summed in order: deterministic for a given
+// launch configuration.  Needs blockDim.x doubles of shared scratch.
 static __device__ void finish_partials(const double* part, int nblk, int n, double* out) {
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    double s = part[e];
-    for (int b = 1; b < nblk; ++b) s += part[size_t(b) * n + e];
-    out[e] = s;
+  __shared__ double seg_sum[1024];
+  const int T = blockDim.x;
+  int segs = T / max(n, 1);
+  segs = max(1, min(segs, min(32, nblk)));
+  if (n * segs <= T) {
+    const int t = threadIdx.x;
+    if (t < n * segs) {
+      const int e = t % n, sg = t / n;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int b = sg;
+      for (; b + 3 * segs < nblk; b += 4 * segs) {
+        a0 += part[size_t(b) * n + e];
+        a1 += part[size_t(b + segs) * n + e];
+        a2 += part[size_t(b + 2 * segs) * n + e];
+        a3 += part[size_t(b + 3 * segs) * n + e];
+      }
+      for (; b < nblk; b += segs) a0 += part[size_t(b) * n + e];
+      seg_sum[sg * n + e] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += T) {
+      double s = seg_sum[e];
+      for (int sg = 1; sg < segs; ++sg) s += seg_sum[sg * n + e];
+      out[e] = s;
+    }
+  } else {
+    for (int e = threadIdx.x; e < n; e += T) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int b = 0;
+      for (; b + 3 < nblk; b += 4) {
+        a0 += part[size_t(b) * n + e];
+        a1 += part[size_t(b + 1) * n + e];
+        a2 += part[size_t(b + 2) * n + e];
+        a3 += part[size_t(b + 3) * n + e];
+      }
+      for (; b < nblk; ++b) a0 += part[size_t(b) * n + e];
+      out[e] = (a0 + a1) + (a2 + a3);
+    }
   }
 }
 
@@ -89,15 +127,13 @@ __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, doub
   const int stride = R + 1;
   for (int e = threadIdx.x; e < stride; e += blockDim.x) part[size_t(blockIdx.x) * stride + e] = colbuf[e];
   if (last_cta_ticket(ticket)) {
-    const int nblk = gridDim.x;
+    finish_partials(part, gridDim.x, stride, colbuf);
+    __syncthreads();
     for (int e = threadIdx.x; e < stride; e += blockDim.x) {
-      if (e == R && !beta) continue;
-      double s = part[e];
-      for (int b = 1; b < nblk; ++b) s += part[size_t(b) * stride + e];
       if (e < R) {
-        if (nsq) nsq[e] = s;
-      } else {
-        beta[0] = s;
+        if (nsq) nsq[e] = colbuf[e];
+      } else if (beta) {
+        beta[0] = colbuf[e];
       }
     }
   }
