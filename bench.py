@@ -140,10 +140,14 @@ def cpu_reference_time(conf, steps, warmup):
     slab = cpu_slab(dims)
     rng = np.random.default_rng(DATA_SEED)
     hs = [rng.random((d, rank)) for d in slab]
-    clean = O.khatri_rao(hs) @ np.ones(rank)
-    rms = float(np.sqrt(np.mean(clean * clean)))
-    data = clean + conf["eta"] * rms * np.abs(rng.standard_normal(clean.size))
-    del clean
+    # sum of rank-one terms built slice by slice (no 2^28 x R Khatri-Rao temporary)
+    lead = math.prod(slab[:-1])
+    krp_lead = O.khatri_rao(hs[:-1])                     # (prod of leading dims, R)
+    data = np.empty(math.prod(slab))
+    for k in range(slab[-1]):
+        data[k * lead:(k + 1) * lead] = krp_lead @ hs[-1][k]
+    rms = float(np.sqrt(np.mean(data * data)))
+    data += conf["eta"] * rms * np.abs(rng.standard_normal(data.size))
     timings = []
     O.run_sequential(data, slab, rank, conf["algo"], max_iters=warmup + steps, tol=0.0, seed=INIT_SEED,
                      timings=timings, init_error="tree")
