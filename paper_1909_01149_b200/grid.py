@@ -211,6 +211,9 @@ class DistCollectives:
         self.dist = dist
         self.layout = layout
         self.counters = CommCounters()
+        # gloo moves host memory only: device tensors are staged through the host
+        # (CPU tests and the single-GPU multi-process test); NCCL works in place.
+        self.stage = dist.get_backend() == "gloo"
         grid = layout.grid
         if dist_groups is None:
             dist_groups = make_slice_process_groups(grid)
@@ -220,7 +223,12 @@ class DistCollectives:
         ops = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}
         if op not in ops:
             raise ValueError(f"unknown reduction {op!r}")
-        self.dist.all_reduce(t, op=ops[op])
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=ops[op])
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=ops[op])
         self.counters.record("AllReduce", t.numel(), t.numel())
         return t
 
@@ -240,8 +248,13 @@ class DistCollectives:
                     blk = parts.block(k)
                     inp[k, : blk.stop - blk.start] = t[blk]
                 inp = inp.reshape(-1)
-            out_full = torch.empty((width, r), dtype=t.dtype, device=t.device)
-            self.dist.reduce_scatter_tensor(out_full.reshape(-1), inp.contiguous(), group=self.slice_pg[mode])
+            if self.stage and t.is_cuda:
+                out_h = torch.empty((width, r), dtype=t.dtype)
+                self.dist.reduce_scatter_tensor(out_h.reshape(-1), inp.contiguous().cpu(), group=self.slice_pg[mode])
+                out_full = out_h.to(t.device)
+            else:
+                out_full = torch.empty((width, r), dtype=t.dtype, device=t.device)
+                self.dist.reduce_scatter_tensor(out_full.reshape(-1), inp.contiguous(), group=self.slice_pg[mode])
             out = out_full[: parts.lengths[me]]
         self.counters.record("ReduceScatter", t.numel(), out.numel())
         return out
@@ -255,8 +268,13 @@ class DistCollectives:
         else:
             src = torch.zeros((width, r), dtype=t.dtype, device=t.device)
             src[: t.shape[0]] = t
-            full = torch.empty((group.size, width, r), dtype=t.dtype, device=t.device)
-            self.dist.all_gather_into_tensor(full.reshape(-1), src.reshape(-1), group=self.slice_pg[mode])
+            if self.stage and t.is_cuda:
+                full_h = torch.empty((group.size, width, r), dtype=t.dtype)
+                self.dist.all_gather_into_tensor(full_h.reshape(-1), src.reshape(-1).cpu(), group=self.slice_pg[mode])
+                full = full_h.to(t.device)
+            else:
+                full = torch.empty((group.size, width, r), dtype=t.dtype, device=t.device)
+                self.dist.all_gather_into_tensor(full.reshape(-1), src.reshape(-1), group=self.slice_pg[mode])
             out = torch.cat([full[k, : parts.lengths[k]] for k in range(group.size)], dim=0)
         self.counters.record("AllGather", t.numel(), out.numel())
         return out
