@@ -176,9 +176,16 @@ def gpu_run(args, conf):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # NNCP_DIST_BACKEND=gloo runs the multi-rank flow on fewer GPUs than ranks (ranks share
+    # devices, host-staged collectives; for checking the path only -- timings are meaningless)
+    backend = os.environ.get("NNCP_DIST_BACKEND", "nccl")
+    dev = local % torch.cuda.device_count() if backend == "gloo" else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     dims, R = conf["dims"], conf["rank"]
     grid = GRIDS[len(dims)][world]
     layout = RankLayout(Grid(grid), rank, dims)
@@ -197,7 +204,7 @@ def gpu_run(args, conf):
             dist.barrier()
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     eng.ctx.kernel_events = []
     launches0 = _lib.load().nncp_launch_count()
     replays0 = eng.graph_replays
