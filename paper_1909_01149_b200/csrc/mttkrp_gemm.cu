@@ -152,7 +152,8 @@ struct LeftTile {
   static constexpr int BM = 256;  // tensor rows (retained leading modes) per CTA
   static constexpr int BK = 16;   // contracted columns per stage
   static constexpr int NF = RP / 8;
-  static constexpr int STAGES = (RP <= 32) ? 5 : 4;
+  // HBM-bound ranks (RP <= 24) keep one more stage in flight
+  static constexpr int STAGES = (RP <= 24) ? 6 : (RP <= 32) ? 5 : 4;
   static constexpr int PRODUCERS = 4;
   static constexpr int THREADS = 256 + 32 * PRODUCERS;
   static constexpr int A_ELEMS = BM * BK;
