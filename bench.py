@@ -250,13 +250,18 @@ def gpu_run(args, conf):
     barrier()
     launches0 = _lib.load().nncp_launch_count()
     t0 = time.perf_counter()
-    xs = host.to("cuda", non_blocking=False)
     cfg_e2e = P.RunConfig(rank=R, algorithm=conf["algo"], max_iters=args.steps, tol=0.0, seed=INIT_SEED,
                           cuda_graph=args.graph and world == 1)
-    eng2, rep2 = P.run_local(xs, layout.local_dims, dims, cfg_e2e,
-                             DistCollectives(layout) if world > 1 else IdentityCollectives(),
-                             layout if world > 1 else None, timing=False)
-    model, lam = eng2.model_host()
+    if world == 1:
+        # the user's call: nncp_sequential on a host (pinned) tensor -> H2D, init, K sweeps, model D2H
+        rep2 = P.nncp_sequential(P.DenseTensor(dims, host), cfg_e2e)
+        model, lam = rep2.model.factors, rep2.model.lam
+    else:
+        xs = host.to("cuda", non_blocking=False)
+        eng2, rep2 = P.run_local(xs, layout.local_dims, dims, cfg_e2e, DistCollectives(layout), layout,
+                                 timing=False)
+        model, lam = eng2.model_host()
+        del eng2, xs
     barrier()
     e2e_wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -266,7 +271,6 @@ def gpu_run(args, conf):
     out["h2d_bytes"] = int(host.numel() * 8)
     out["d2h_bytes"] = int(sum(m.size for m in model) * 8 + lam.size * 8 + 16 * args.steps)
     out["e2e_errors"] = list(rep2.errors)
-    del eng2, xs
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -364,7 +368,8 @@ def main():
         "e2e": {"value": res["e2e_s"] / args.steps, "unit": "s/iter",
                 "h2d_bytes_per_step": res["h2d_bytes"] // args.steps,
                 "d2h_bytes_per_step": res["d2h_bytes"] // args.steps,
-                "note": "run_local/nncp_sequential path from pinned host memory: tensor H2D once per call of "
+                "note": "nncp_sequential(DenseTensor(pinned host tensor)) (N>1: per-rank block through the "
+                        "engine): tensor H2D once per call of "
                         f"{args.steps} iterations + init + D2H of the model, divided by the steps"},
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
