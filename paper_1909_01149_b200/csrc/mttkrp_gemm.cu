@@ -386,13 +386,16 @@ __global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
         blo[j] = bs[((2 * k8) * NF + j) * 32];
         bhi[j] = bs[((2 * k8 + 1) * NF + j) * 32];
       }
+      // all independent "lo" products first: back-to-back lo/hi on one accumulator
+      // would serialise on the DMMA latency (the asm statements are not reordered)
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          dmma884(acc[f][j][0], acc[f][j][1], alo[f], blo[j]);
-          dmma884(acc[f][j][0], acc[f][j][1], ahi[f], bhi[j]);
-        }
+        for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], alo[f], blo[j]);
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) dmma884(acc[f][j][0], acc[f][j][1], ahi[f], bhi[j]);
     }
     pending = s;
   }

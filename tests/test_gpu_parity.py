@@ -94,7 +94,9 @@ def test_dimtree_order_errors(P):
 
 
 @pytest.mark.parametrize("dims,r", [((128, 96, 80), 32), ((64, 48, 40, 24), 16), ((4096, 64, 32), 20),
-                                    ((100, 64, 64), 64), ((256, 256, 300), 8), ((7, 9, 11), 5)])
+                                    ((100, 64, 64), 64), ((256, 256, 300), 8), ((7, 9, 11), 5),
+                                    ((96, 64, 48), 40), ((64, 64, 64, 8), 48), ((130, 70, 50), 56),
+                                    ((30, 20, 10, 8, 6), 12), ((2, 3, 4, 5, 6, 7), 3)])
 def test_partials_vs_oracle_larger(P, dims, r):
     rng = np.random.default_rng(sum(dims) + r)
     x = rng.random(int(np.prod(dims)))
