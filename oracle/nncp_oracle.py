@@ -3,8 +3,9 @@
 This module is a numpy restatement of the reference package's algorithm
 (`/root/reference/pkg/src/nncp`, pure Python + numpy/OpenBLAS) for the one
 path this repository accelerates: dimension-tree MTTKRP, Gram/Hadamard
-normal equations, the MU / HALS / ANLS-BPP factor updates, column
-normalisation and the Gram-trick relative error.  Only ``tests/``,
+normal equations, the MU / HALS / ANLS-BPP factor updates (plus UCP, ADMM and
+Nesterov with outer extrapolation, the widened rows), column normalisation
+and the Gram-trick relative error.  Only ``tests/``,
 ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
 ``--impl reference`` legs may import it, and only as the checker or the
 timed CPU baseline ("port").  The product path (``paper_1909_01149_b200``)
@@ -269,7 +270,86 @@ def bpp_update(s, m, cur=None):
     return out
 
 
+ADMM_INNER_CAP = 5          # updaters.py:25
+NESTEROV_INNER_CAP = 20     # updaters.py:26
+
+
+def ucp_update(s, m, cur=None):
+    """Unconstrained Cholesky solve with the ridge fallback (updaters.py:77-88)."""
+    from scipy.linalg import LinAlgError, cho_factor, cho_solve
+
+    try:
+        return cho_solve(cho_factor(s), m.T).T
+    except LinAlgError:
+        warnings.warn("singular gram in unconstrained update, adding ridge")
+        ridge = 1e-12 * np.trace(s) / s.shape[0]
+        try:
+            return cho_solve(cho_factor(s + ridge * np.eye(s.shape[0])), m.T).T
+        except LinAlgError:
+            return np.linalg.lstsq(s, m.T, rcond=None)[0].T
+
+
+def admm_update(s, m, cur, dual, rho=None, max_steps=ADMM_INNER_CAP, rtol=1e-4, reduce=lambda v: v):
+    """Three-step ADMM splitting, returns (x, dual, steps) (updaters.py:167-220)."""
+    from scipy.linalg import cho_factor, cho_solve
+
+    r = s.shape[0]
+    if rho is None:
+        rho = float(np.trace(s)) / r
+        rho = rho if rho > 0.0 else 1.0
+    chol = cho_factor(s + rho * np.eye(r))
+    x = cur
+    u = np.zeros_like(cur) if dual is None else dual
+    steps = 0
+    for _ in range(max_steps):
+        xhat = cho_solve(chol, (m + rho * (x + u)).T).T
+        xprev = x
+        x = np.maximum(xhat - u, 0.0)
+        u = u + x - xhat
+        steps += 1
+        sq = reduce(np.array([np.sum((x - xhat) ** 2), np.sum(x ** 2), np.sum(xhat ** 2),
+                              np.sum((x - xprev) ** 2), np.sum(u ** 2)]))
+        gap, nx, nxhat, step, nu = np.sqrt(sq)
+        if gap <= rtol * max(nx, nxhat) and rho * step <= rtol * nu * rho:
+            break
+    return x, u, steps
+
+
+def nesterov_hyperparams(s, prox_floor=1e-6):
+    """(lam, alpha, beta) from the Gram spectrum (updaters.py:223-243)."""
+    ev = np.linalg.eigvalsh(s)
+    big, small = float(ev[-1]), max(float(ev[0]), 0.0)
+    if big <= 0.0:
+        lam = 1.0
+    elif small / big >= prox_floor:
+        lam = 0.0
+    else:
+        lam = (prox_floor * big - small) / (1.0 - prox_floor)
+    q = (small + lam) / (big + lam)
+    return lam, 1.0 / (big + lam), (1.0 - np.sqrt(q)) / (1.0 + np.sqrt(q))
+
+
+def nesterov_update(s, m, cur, xstar, max_iters=NESTEROV_INNER_CAP, tol=1e-8, reduce=lambda v: v):
+    """Accelerated projected gradient with proximal centre (updaters.py:250-281); returns (x, steps)."""
+    lam, alpha, beta = nesterov_hyperparams(s)
+    xstar = cur if xstar is None else xstar
+    x = y = cur
+    steps = 0
+    for _ in range(max_iters):
+        grad = y @ s - m + lam * (y - xstar)
+        xn = np.maximum(y - alpha * grad, 0.0)
+        steps += 1
+        dmax, xmax = reduce(np.array([np.max(np.abs(xn - x)) if xn.size else 0.0,
+                                      np.max(np.abs(xn)) if xn.size else 0.0]))
+        y = xn + beta * (xn - x)
+        x = xn
+        if dmax <= tol * (1.0 + xmax):
+            break
+    return x, steps
+
+
 UPDATERS = {"mu": lambda s, m, c: mu_update(s, m, c),
+            "ucp": lambda s, m, c: ucp_update(s, m, c),
             "hals": lambda s, m, c: hals_update(s, m, c),
             "bpp": lambda s, m, c: bpp_update(s, m, c)}
 
@@ -302,7 +382,7 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
     dims = tuple(int(d) for d in dims)
     order = len(dims)
     data = np.ascontiguousarray(data, dtype=np.float64).ravel()
-    upd = UPDATERS[algorithm]
+    upd = UPDATERS.get(algorithm)
     t0 = time.perf_counter()
     alpha = float(np.dot(data, data))
     if alpha <= 0.0:
@@ -315,6 +395,8 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
         lam = np.ones(rank)
     grams = [gram(h) for h in hs]
     tree = DimTree(dims, rank, strict_split) if use_dimtree else None
+    duals = [None] * order          # ADMM state per mode (updaters.py:56-68)
+    centres = [None] * order        # Nesterov proximal centre per mode
     if init_error == "naive":
         m0 = naive_mttkrp(data, dims, hs, order - 1)
     else:  # same quantity through the tree's last-mode path (bench baseline: init is not timed)
@@ -326,13 +408,21 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
         timings.append(time.perf_counter() - t0)
     for it in range(1, max_iters + 1):
         t0 = time.perf_counter()
+        if algorithm == "nes":
+            prev_hs, prev_lam = [h.copy() for h in hs], lam.copy()
         if tree is not None:
             tree.begin_iteration()
         for n in range(order):
             mb = tree.mttkrp(data, hs, n) if tree is not None else naive_mttkrp(data, dims, hs, n)
             s_n = hadamard_excluding(grams, n)
             try:
-                hhat = upd(s_n, mb, hs[n] * lam)
+                if algorithm == "admm":
+                    hhat, duals[n], _ = admm_update(s_n, mb, hs[n] * lam, duals[n])
+                elif algorithm == "nes":
+                    hhat, _ = nesterov_update(s_n, mb, hs[n] * lam, centres[n])
+                    centres[n] = hhat.copy()
+                else:
+                    hhat = upd(s_n, mb, hs[n] * lam)
             except Exception as exc:
                 raise RuntimeError(f"NNLS update failed at iteration {it}, mode {n + 1}") from exc
             w = np.sqrt(np.sum(hhat * hhat, axis=0))
@@ -345,12 +435,35 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
         gamma = float(lam @ ((s_last * grams[-1]) @ lam))
         eps = eps_from_terms(alpha, beta, gamma)
         errors.append(eps)
+        if algorithm == "nes":
+            hs, lam, grams = _nes_accelerate(data, dims, tree, it, eps, alpha, hs, lam, grams, prev_hs,
+                                             prev_lam, use_dimtree)
         if timings is not None:
             timings.append(time.perf_counter() - t0)
         if eps <= tol:
             break
     calls = tree.partial_calls if tree is not None else 0
     return errors, hs, lam, (tree.split if tree is not None else None), calls
+
+
+def _nes_accelerate(data, dims, tree, it, eps, alpha, hs, lam, grams, prev_hs, prev_lam, use_dimtree):
+    """Outer extrapolation, accepted only if strictly better (driver.py:452-492, 310-328)."""
+    step = float(it) ** (1.0 / len(hs))
+    cand = [np.maximum(h + step * (h - hp), 0.0) for h, hp in zip(hs, prev_hs)]
+    cand_lam = np.maximum(lam + step * (lam - prev_lam), 0.0)
+    if use_dimtree:
+        mb = tree.mttkrp_last_mode(data, cand)
+    else:
+        mb = naive_mttkrp(data, dims, cand, len(dims) - 1)
+    beta = float(np.dot(mb.ravel(), (cand[-1] * cand_lam).ravel()))
+    cg = [h.T @ h for h in cand]
+    gamma = float(cand_lam @ (np.prod(cg, axis=0) @ cand_lam))
+    if not eps_from_terms(alpha, beta, gamma) < eps:
+        return hs, lam, grams
+    w = np.sqrt(np.stack([np.sum(h * h, axis=0) for h in cand]))
+    scale = np.where(w > 0.0, w, 1.0)
+    new = [h / scale[n] for n, h in enumerate(cand)]
+    return new, cand_lam * np.prod(w, axis=0), [gram(h) for h in new]
 
 
 def reconstruct(factors, lam) -> np.ndarray:

@@ -139,3 +139,27 @@ def test_error_identity_vs_reconstruction():
         x = rng.random(int(np.prod(dims))) + 0.01
         errors, hs, lam, _, _ = O.run_sequential(x, dims, 2, "hals", 3, 0.0, 1)
         assert abs(errors[-1] - O.relative_error_direct(x, hs, lam)) <= 1e-8
+
+
+def test_oracle_stateful_vs_golden(golden):
+    """UCP / ADMM / NES restatements pinned to the live reference (tests/golden/stateful.npz)."""
+    g = golden("stateful.npz")
+    for k in range(int(g["nst"])):
+        s, m, cur = g[f"s{k}_s"], g[f"s{k}_m"], g[f"s{k}_cur"]
+        assert rel_fro(O.ucp_update(s, m), g[f"s{k}_ucp"]) <= 1e-12
+        x1, u, steps = O.admm_update(s, m, cur, None)
+        assert steps == int(g[f"s{k}_admm1_iters"]) and rel_fro(x1, g[f"s{k}_admm1"]) <= 1e-12
+        x2, u, _ = O.admm_update(s, m, x1, u)
+        assert rel_fro(x2, g[f"s{k}_admm2"]) <= 1e-12 and rel_fro(u, g[f"s{k}_admm_dual"]) <= 1e-12
+        xn, steps = O.nesterov_update(s, m, cur, None)
+        assert steps == int(g[f"s{k}_nes_iters"]) and rel_fro(xn, g[f"s{k}_nes"]) <= 1e-12
+        assert np.allclose(O.nesterov_hyperparams(s), g[f"s{k}_hyper"], rtol=1e-14, atol=0)
+    for name in [str(n) for n in g["runs"]]:
+        dims = tuple(int(d) for d in g[f"{name}_dims"])
+        r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            errors, hs, lam, _, calls = O.run_sequential(g[f"{name}_x"], dims, r, str(g[f"{name}_algo"]), iters,
+                                                         0.0, iseed)
+        assert np.max(np.abs(np.array(errors) - g[f"{name}_errors"])) <= 1e-12, name
+        assert calls == int(g[f"{name}_partials"]), name
