@@ -194,7 +194,7 @@ def gpu_run(args, conf):
     x_local = synthetic_block(dims, fs, conf["eta"], DATA_SEED, offsets=offs, local_dims=layout.local_dims)
     coll = DistCollectives(layout) if world > 1 else IdentityCollectives()
     cfg = P.RunConfig(rank=R, algorithm=conf["algo"], max_iters=args.warmup + args.steps + 1, tol=0.0,
-                      seed=INIT_SEED, cuda_graph=args.graph and world == 1)
+                      seed=INIT_SEED, cuda_graph=False if args.eager else None)
     eng = _Engine(x_local, layout.local_dims, dims, cfg, coll, layout if world > 1 else None, timing=False)
     eng.initialise()
     eng.iterate(args.warmup)
@@ -251,7 +251,7 @@ def gpu_run(args, conf):
     launches0 = _lib.load().nncp_launch_count()
     t0 = time.perf_counter()
     cfg_e2e = P.RunConfig(rank=R, algorithm=conf["algo"], max_iters=args.steps, tol=0.0, seed=INIT_SEED,
-                          cuda_graph=args.graph and world == 1)
+                          cuda_graph=False if args.eager else None)
     if world == 1:
         # the user's call: nncp_sequential on a host (pinned) tensor -> H2D, init, K sweeps, model D2H
         rep2 = P.nncp_sequential(P.DenseTensor(dims, host), cfg_e2e)
@@ -284,7 +284,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--graph", action="store_true", help="replay each sweep as a CUDA graph")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every kernel from the host each sweep (default: replay the sweep as a CUDA graph)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -14,7 +14,8 @@ Public surface identical to the reference (driver.py:46-56, 73-134, 495-531):
     per sweep:   All-Reduce(beta), gamma kernel, one 2-scalar + status D2H
 
 Host work per iteration is kernel launches plus that one small read-back;
-optionally the whole sweep is replayed as a CUDA graph (``cuda_graph=True``).
+by default the whole sweep is replayed as a CUDA graph after the first one
+(``RunConfig.cuda_graph``).
 Category seconds come from CUDA events on the launching stream.
 """
 
@@ -47,7 +48,14 @@ FUSED_ALGORITHMS = ("mu", "hals", "bpp", "ucp")   # one kernel per mode (CUDA-gr
 
 @dataclass
 class RunConfig:
-    """Knobs of one decomposition run (driver.py:73-101); ``cuda_graph`` is device-only."""
+    """Knobs of one decomposition run (driver.py:73-101).
+
+    ``cuda_graph`` (device-only): after the first sweep, the whole sweep of
+    launches (including the per-category timing events) is replayed as one
+    CUDA graph.  ``None`` (default) enables it whenever the sweep is
+    capturable (one execution context, MU/HALS/BPP/UCP); ``False`` forces
+    eager launches.
+    """
 
     rank: int
     algorithm: str = "bpp"
@@ -58,7 +66,7 @@ class RunConfig:
     use_dimtree: bool = True
     strict_split: bool = False
     initial_factors: FactorSet = None
-    cuda_graph: bool = False
+    cuda_graph: bool = None   # None = auto: replay the sweep as a CUDA graph when it is capturable
 
     def validate(self, order: int):
         if self.rank < 1:
@@ -158,11 +166,34 @@ class _EventTimer:
         self._pool = []
         self._marks = []
         self._start = None
+        self.capturing = False          # marks become event-record nodes of the sweep graph
+        self.graph_marks = None         # (start, [(category, event), ...]) of the captured sweep
 
     def _event(self):
+        if self.capturing:
+            return torch.cuda.Event(enable_timing=True, external=True)
         if self._pool:
             return self._pool.pop()
         return torch.cuda.Event(enable_timing=True)
+
+    def begin_capture(self):
+        self.capturing = True
+        self.start()
+
+    def end_capture(self):
+        if self.enabled:
+            self.graph_marks = (self._start, list(self._marks))
+        self._marks, self._start = [], None
+        self.capturing = False
+
+    def collect_graph(self, row: dict):
+        """Per-category seconds of the last graph replay (after the stream is synchronised)."""
+        if not self.enabled or self.graph_marks is None:
+            return
+        prev, marks = self.graph_marks
+        for cat, e in marks:
+            row[cat] += prev.elapsed_time(e) / 1e3
+            prev = e
 
     def start(self):
         if not self.enabled:
@@ -251,6 +282,7 @@ class _Engine:
                 self.runner = NesterovRunner(rows_max, R, dev, self.ws)
                 self.nes_prev = [None] * N
         self.graph = None
+        self.graph_failed = False
         self.graph_kernels = 0      # library kernels captured in the sweep graph
         self.graph_replays = 0
         self.report = RunReport()
@@ -476,13 +508,14 @@ class _Engine:
         """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
         cfg = self.cfg
         errors = self.report.errors
-        use_graph = cfg.cuda_graph and not self.coll.parallel and cfg.algorithm in FUSED_ALGORITHMS
+        capturable = not self.coll.parallel and cfg.algorithm in FUSED_ALGORITHMS
+        use_graph = capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
         for it in range(done + 1, stop + 1):
             self.report.begin_row()
             wall0 = time.perf_counter()
-            if use_graph and self.graph is None and it > 1:
+            if use_graph and self.graph is None and it > 1 and not self.graph_failed:
                 self._capture()
             if self.graph is not None:
                 self.graph.replay()
@@ -495,7 +528,10 @@ class _Engine:
                     self._snapshot()
                 self._sweep()
             eps = self._finish_iteration(it)
-            self.timer.collect(self.report.rows[-1])
+            if self.graph is not None:
+                self.timer.collect_graph(self.report.rows[-1])
+            else:
+                self.timer.collect(self.report.rows[-1])
             errors.append(eps)
             if cfg.algorithm == "nes":
                 self._nes_accelerate(it, eps)
@@ -508,21 +544,28 @@ class _Engine:
 
     def _capture(self):
         """Record one sweep as a CUDA graph (all buffers already allocated by sweep 1)."""
-        timing = self.timer.enabled
-        self.timer.enabled = False
         calls = self.ctx.partial_calls
         launches0 = self.lib.nncp_launch_count()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
-                self._sweep()
+        try:
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    self.timer.begin_capture()
+                    self._sweep()
+                    self.timer.end_capture()
+        except Exception as exc:  # noqa: BLE001  (stay on the eager path, still correct)
+            self.timer.capturing = False
+            warnings.warn(f"CUDA graph capture failed, continuing without graphs: {exc}")
+            torch.cuda.current_stream().wait_stream(side)
+            self.ctx.partial_calls = calls
+            self.graph_failed = True
+            return
         torch.cuda.current_stream().wait_stream(side)
         self.ctx.partial_calls = calls
         self.graph_kernels = int(self.lib.nncp_launch_count() - launches0)
         self.graph = g
-        self.timer.enabled = timing
 
     def model_host(self):
         return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()

@@ -186,7 +186,7 @@ def test_sequential_runs_vs_golden(P, golden):
 def test_cuda_graph_matches_eager(P, golden):
     g = golden("runs.npz")
     for name in ("c1_mu", "hals_r16", "bpp4"):
-        _, _, _, _, x, cfg = _run_case(P, g, name)
+        _, _, _, _, x, cfg = _run_case(P, g, name, cuda_graph=False)
         eager = P.nncp_sequential(x, cfg)
         _, _, _, _, x, cfg = _run_case(P, g, name, cuda_graph=True)
         graph = P.nncp_sequential(x, cfg)
@@ -194,6 +194,8 @@ def test_cuda_graph_matches_eager(P, golden):
         for a, b in zip(eager.model.factors, graph.model.factors):
             assert np.array_equal(a, b)
         assert graph.tree_partial_calls == eager.tree_partial_calls
+        # per-category device seconds are recorded inside the graph as well
+        assert all(sum(row.values()) > 0 for row in graph.rows[1:])
 
 
 def test_run_to_run_determinism(P, golden):
