@@ -53,7 +53,7 @@ def _worker(rank, world, port, case, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [("hals_odd", (2, 2, 1)), ("mu4", (2, 1, 2, 1))])
+@pytest.mark.parametrize("case", [("hals_odd", (2, 2, 1)), ("mu4", (2, 1, 2, 1)), ("bpp3", (2, 2, 2))])
 def test_spmd_processes_match_reference_grid_run(golden, case):
     import torch
     import torch.multiprocessing as mp
