@@ -68,7 +68,7 @@ def test_spmd_processes_match_reference_grid_run(golden, case):
     procs = [ctx.Process(target=_worker, args=(k, world, port, case, q)) for k in range(world)]
     for p in procs:
         p.start()
-    results = dict((item[0], item[1:]) for item in (q.get(timeout=300) for _ in range(world)))
+    results = dict((item[0], item[1:]) for item in (q.get(timeout=900) for _ in range(world)))
     for p in procs:
         p.join(timeout=120)
     g = golden("runs.npz")
