@@ -100,29 +100,49 @@ struct KrpCursor {
 // is >= hi or the column >= R).  Multiplication order ((H_a * H_b) * H_c) is
 // khatri_rao's (tensor_ops.py:121-137).
 template <int NF, int U, int NFM>
-__device__ __forceinline__ void produce_krp(const KrpSpec& krp, const KrpCursor<U, NFM>& cur,
-                                            double* __restrict__ bdst, int lane, int R, int64_t hi) {
+struct KrpRaw {
+  double f[U][NFM][NF];  // raw factor entries of one stage, loaded ahead of their use
+};
+
+// Issue every factor load of one stage (no use yet: the loads stay in flight while
+// the producer waits for the stage's empty barrier).
+template <int NF, int U, int NFM>
+__device__ __forceinline__ void krp_load(const KrpSpec& krp, const KrpCursor<U, NFM>& cur, int lane, int R,
+                                         int64_t hi, KrpRaw<NF, U, NFM>& raw) {
   const int g = lane >> 2;
-  double v[U][NF];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool in = cur.k[u] < hi;
-#pragma unroll
-    for (int j = 0; j < NF; ++j) v[u][j] = 1.0;
 #pragma unroll
     for (int f = 0; f < NFM; ++f) {
       if (f < KrpCursor<U, NFM>::count(krp)) {
         const double* base = krp.ptr[f] + (in ? int64_t(cur.dig[u][f]) * R : 0);
 #pragma unroll
-        for (int j = 0; j < NF; ++j) v[u][j] *= __ldg(base + min(8 * j + g, R - 1));
+        for (int j = 0; j < NF; ++j) raw.f[u][f][j] = __ldg(base + min(8 * j + g, R - 1));
       }
     }
   }
+}
+
+// Multiply the raw entries into KRP values (order (H_a * H_b) * H_c, as khatri_rao)
+// and write them in the fragment-native layout: k4-step u, n-fragment j, lane (g, c)
+// holds KRP[row(u, c)][8j + g]; zero outside the row range or beyond R.
+template <int NF, int U, int NFM>
+__device__ __forceinline__ void krp_store(const KrpSpec& krp, const KrpCursor<U, NFM>& cur,
+                                          const KrpRaw<NF, U, NFM>& raw, double* __restrict__ bdst, int lane, int R,
+                                          int64_t hi) {
+  const int g = lane >> 2;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool in = cur.k[u] < hi;
 #pragma unroll
-    for (int j = 0; j < NF; ++j) bdst[(u * NF + j) * 32 + lane] = (in && 8 * j + g < R) ? v[u][j] : 0.0;
+    for (int j = 0; j < NF; ++j) {
+      double v = 1.0;
+#pragma unroll
+      for (int f = 0; f < NFM; ++f)
+        if (f < KrpCursor<U, NFM>::count(krp)) v *= raw.f[u][f][j];
+      bdst[(u * NF + j) * 32 + lane] = (in && 8 * j + g < R) ? v : 0.0;
+    }
   }
 }
 
@@ -205,6 +225,8 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
       const int nchunks = int((ke - kb + BK - 1) / BK);
       KrpCursor<UP, NFM> cur;
       cur.init(krp, [&](int t, int cc) { return kb + 4 * (t + pw * UP) + cc; }, lane & 3);
+      KrpRaw<NF, UP, NFM> raw;
+      krp_load<NF, UP, NFM>(krp, cur, lane, R, ke, raw);
       for (int ch = 0; ch < nchunks; ++ch, ++gch) {
         const int s = int(gch % ST);
         if (gch >= uint32_t(ST)) mbar_wait(&empty[s], ((gch / ST) - 1) & 1);
@@ -214,9 +236,10 @@ __global__ void __launch_bounds__(LeftTile<RP>::THREADS, 1)
           mbar_arrive_expect_tx(&full[s], uint32_t(T::A_ELEMS * 8));
           tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(m0), int(k0));
         }
-        produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, ke);
-        cur.advance(krp, BK);
+        krp_store<NF, UP, NFM>(krp, cur, raw, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, ke);
         mbar_arrive(&full[s]);
+        cur.advance(krp, BK);
+        if (ch + 1 < nchunks) krp_load<NF, UP, NFM>(krp, cur, lane, R, ke, raw);  // next stage, in flight
       }
     }
     // producer tail: stay resident until the consumers released every stage
@@ -340,6 +363,8 @@ __global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
       const int uu = u + pw * UP;
       return mb + 8 * (uu >> 1) + 2 * cc + (uu & 1);
     }, lane & 3);
+    KrpRaw<NF, UP, NFM> raw;
+    krp_load<NF, UP, NFM>(krp, cur, lane, R, me, raw);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch % ST;
       if (ch >= ST) mbar_wait(&empty[s], ((ch / ST) - 1) & 1);
@@ -350,9 +375,10 @@ __global__ void __launch_bounds__(RightTile<RP>::THREADS, 1)
         tma_load_2d(As + s * T::A_ELEMS, &xmap, &full[s], int(mc), int(j0));
       }
       // k4-step u: fragment column c <-> m = 8 (u/2) + 2c + (u&1)
-      produce_krp<NF, UP, NFM>(krp, cur, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, me);
-      cur.advance(krp, BMC);
+      krp_store<NF, UP, NFM>(krp, cur, raw, Bs + s * T::B_ELEMS + pw * UP * NF * 32, lane, R, me);
       mbar_arrive(&full[s]);
+      cur.advance(krp, BMC);
+      if (ch + 1 < nchunks) krp_load<NF, UP, NFM>(krp, cur, lane, R, me, raw);  // next stage, in flight
     }
     // producer tail: stay resident until the consumers released every stage
     for (int ch = max(0, nchunks - ST); ch < nchunks; ++ch) mbar_wait(&empty[ch % ST], (ch / ST) & 1);
