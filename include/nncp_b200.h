@@ -84,6 +84,22 @@ int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int spl
                         const double* const* factors, int rank, double* out, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* Sliced-tensor partial MTTKRP (same contraction as nncp_partial_mttkrp, on the
+ * int8 tensor cores: tcgen05.mma kind::i8, Ozaki-scheme digit slices).
+ * The tensor is sliced ONCE (nncp_slice_tensor) for a fixed split; every later
+ * partial reads `levels` int8 digit planes (levels bytes per element) instead of
+ * the fp64 tensor.  levels: 6 (46-bit operands) or 7 (54-bit).
+ * nncp_sliced_tensor_bytes: device buffer size for nncp_slice_tensor (host out).
+ * nncp_sliced_workspace_bytes: workspace of nncp_partial_mttkrp_sliced (both sides),
+ * 0 for an invalid shape.  Buffers are used from their first 1 KB boundary on. */
+int nncp_sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels, size_t* bytes);
+int nncp_slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                      size_t bytes, void* stream);
+size_t nncp_sliced_workspace_bytes(int order, const int64_t* dims, int split, int rank, int levels);
+int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dims, int split, int side,
+                               const double* const* factors, int rank, int levels, double* out, void* ws,
+                               size_t ws_bytes, void* stream);
+
 /* dimtree.py:135-175 multi_ttv.  temp: column-major (prod(ret_dims), R).
  * TRAILING: coeff = KRP(coeff[0..ncoeff)) with coeff_rows[k] rows each, whose
  *   product must equal prod(ret_dims[1:]); out retains ret_dims[0].

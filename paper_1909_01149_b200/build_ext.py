@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libnncp_b200.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["abi.cu", "mttkrp_gemm.cu", "ttv.cu", "nnls.cu", "nnls_iter.cu", "synth.cu"]
+SOURCES = ["abi.cu", "mttkrp_gemm.cu", "mttkrp_sliced.cu", "ttv.cu", "nnls.cu", "nnls_iter.cu", "synth.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

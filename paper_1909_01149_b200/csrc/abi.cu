@@ -49,6 +49,20 @@ int colsumsq(const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int synthetic(double*, int, const int64_t*, const int64_t*, const int64_t*, const double* const*, int, double,
               uint64_t, cudaStream_t);
 
+size_t sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels);
+size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int levels);
+int slice_tensor(const double*, int, const int64_t*, int, int, void*, size_t, cudaStream_t);
+int sliced_partial_mttkrp(const void*, int, const int64_t*, int, int, const double* const*, int, int, double*, void*,
+                          size_t, cudaStream_t);
+
+// caller buffers for the sliced path are used from the next 1 KB boundary on
+static inline void* align1k(const void* p, size_t bytes, size_t* avail) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023);
+  const size_t skip = a - reinterpret_cast<uintptr_t>(p);
+  *avail = bytes > skip ? bytes - skip : 0;
+  return reinterpret_cast<void*>(a);
+}
+
 static int check_common(int order, const int64_t* dims, int rank) {
   if (order < 2 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "tensor order must be in [2, 8]");
   if (rank < 1) return fail(NNCP_ERR_VALUE, "rank must be at least 1");
@@ -113,6 +127,47 @@ int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int spl
   // the partial kernels use the first 256 bytes of nothing: split-K partials start at ws
   return partial_mttkrp(x, order, dims, split, side, factors, rank, out, ws ? static_cast<char*>(ws) + 256 : nullptr,
                         ws_bytes > 256 ? ws_bytes - 256 : 0, S(stream));
+}
+
+int nncp_sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels, size_t* bytes) {
+  int rc = check_common(order, dims, 1);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (levels != 6 && levels != 7) return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP supports 6 or 7 digit levels");
+  *bytes = 1024 + sliced_tensor_bytes(order, dims, split, levels);
+  return NNCP_OK;
+}
+
+int nncp_slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                      size_t bytes, void* stream) {
+  int rc = check_common(order, dims, 1);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (!x || !sliced) return fail(NNCP_ERR_VALUE, "null tensor or sliced buffer");
+  size_t avail = 0;
+  void* base = align1k(sliced, bytes, &avail);
+  return slice_tensor(x, order, dims, split, levels, base, avail, S(stream));
+}
+
+size_t nncp_sliced_workspace_bytes(int order, const int64_t* dims, int split, int rank, int levels) {
+  if (order < 2 || order > kMaxOrder || rank < 1 || rank > kMaxRank || split < 1 || split >= order) return 0;
+  return 256 + 1024 + sliced_ws_bytes(order, dims, split, rank, levels);
+}
+
+int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dims, int split, int side,
+                               const double* const* factors, int rank, int levels, double* out, void* ws,
+                               size_t ws_bytes, void* stream) {
+  int rc = check_common(order, dims, rank);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (side != NNCP_SIDE_LEFT && side != NNCP_SIDE_RIGHT)
+    return fail(NNCP_ERR_VALUE, "side must be 'left' or 'right'");
+  if (!sliced) return fail(NNCP_ERR_VALUE, "null sliced tensor");
+  size_t dummy = 0, avail = 0;
+  const void* base = align1k(sliced, 1024, &dummy);
+  // the first 256 workspace bytes hold the reduction tickets of the other kernels
+  void* w = (ws && ws_bytes > 256) ? align1k(static_cast<char*>(ws) + 256, ws_bytes - 256, &avail) : nullptr;
+  return sliced_partial_mttkrp(base, order, dims, split, side, factors, rank, levels, out, w, avail, S(stream));
 }
 
 int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, int side,

@@ -56,6 +56,12 @@ inline int num_sms() {
   return sms;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn();
+
 inline int pad8(int r) { return (r + 7) / 8 * 8; }
 
 // ------------------------------------------------------------- device PTX --

@@ -480,12 +480,6 @@ __global__ void splitk_reduce(const double* __restrict__ part, int splits, int64
 }
 
 // ------------------------------------------------------------- host side ---
-namespace {
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
@@ -497,6 +491,8 @@ EncodeTiledFn encode_fn() {
   }
   return fn;
 }
+
+namespace {
 
 int make_map_2d(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                 uint32_t box_outer) {

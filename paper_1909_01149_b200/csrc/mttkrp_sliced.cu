@@ -1,0 +1,914 @@
+// Sliced-operand partial MTTKRP on the int8 tensor cores (tcgen05.mma kind::i8).
+//
+// Same contraction as mttkrp_gemm.cu (dimtree.py:102-127):
+//   left : T_L[m, r] = sum_j X[m + M j] * KRP(H_{S+1..N})[j, r]
+//   right: T_R[j, r] = sum_m X[m + M j] * KRP(H_{1..S})[m, r]
+// computed as an exact integer GEMM over fixed-point digit slices (the Ozaki
+// scheme), because FP64 has no tcgen05 kind and DMMA (37 TF/s) caps the FP64
+// path below the HBM roofline at R >= 23:
+//
+//   * X_(1:S) is sliced ONCE per run (the tensor is constant across ALS
+//     iterations): row m gets a power-of-two scale 2^ex[m] >= max_j |X[m, j]|,
+//     and X[m, j] / 2^ex[m] is rounded to 8L-2 fractional bits and written as L
+//     balanced base-256 digits d_s in [-128, 127] (one int8 plane per digit):
+//       X[m, j] ~= 2^ex[m] * sum_s d_s[m, j] 2^(-8s-6)      |error| <= 2^(ex-8L+1)
+//   * the factor side B (the Khatri-Rao rows; for the right side scaled by
+//     2^ex[m]) is sliced per call with one exponent per (column r, contraction
+//     chunk of <= 16384 rows);
+//   * per contraction chunk the tensor cores accumulate, exactly in int32 TMEM
+//     columns, the L "levels" l = s + t < L of digit products.  One MMA per X
+//     digit s covers all its partners t at once: B's digit planes are
+//     concatenated along N, so  D[:, s*RP .. L*RP) += A_s * [B_0 | .. | B_{L-1-s}];
+//   * an epilogue warpgroup converts each chunk's levels to fp64,
+//     sum_l acc_l 2^(-8l-12) * 2^(ex + eb), and accumulates in registers (fixed
+//     order: bitwise deterministic run to run).
+// Products and sums in the MMA are exact; the only rounding is the digit
+// truncation (relative 2^(1-8L) of the row / column-chunk maxima) and the fp64
+// epilogue (DESIGN.md §4.4 for the bound and the parity tolerance it meets).
+//
+// HBM layout of the digit planes: 128 x 128 blocks, block (mb, jb) holding
+// rows m in [128 mb, +128) and columns j in [128 jb, +128) of every plane as
+// L contiguous 16 KB tiles ([s][j % 128][m % 128]); blocks ordered (mb, jb).
+// One tile is one A operand stage of BOTH sides -- MN-major for the left
+// (m contiguous = the MMA's M), K-major for the right (m = the contraction) --
+// and every TMA request is one contiguous 16 KB run of HBM.  The left streams
+// its m block's 96 KB blocks back to back; the right streams 96 KB per k step.
+// Bytes per partial: L per tensor element (6 at L = 6) instead of fp64's 8.
+//
+// Kernel anatomy (one CTA per SM, persistent over output tiles / split-K items):
+//   warp 0      TMA producer: per 128-deep k block one B stage (the L*RP digit
+//               rows, 128 B each) and L A stages (one digit plane tile each);
+//   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma, commits to
+//               mbarriers: stage release and accumulator-ready);
+//   warps 2..5  epilogue: tcgen05.ld of the level accumulators (double-buffered in
+//               TMEM when 2 L RP <= 512 columns), fp64 conversion, output stores.
+#include "common.cuh"
+
+namespace nncp {
+namespace sliced {
+
+constexpr int BM = 128;                 // UMMA M: output rows per tile
+constexpr int BK = 128;                 // contraction elements (int8 bytes) per k block
+constexpr int TILE = BM * BK;           // bytes of one digit-plane tile (16 KB)
+constexpr int64_t KC_MAX = 16384;       // contraction chunk between int32 -> fp64 conversions
+                                        // (multiple of 256; L * 2^14 * KC_MAX < 2^31 keeps int32 exact)
+constexpr int THREADS = 192;
+constexpr int MAX_SMEM = 227 * 1024;
+
+__host__ __device__ constexpr int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// ----------------------------------------------------------------- layout --
+struct TensorLayout {
+  int64_t M, J, Mp, Jp, nmb, njb;
+  int L;
+  size_t rmax_off, plane_off, total;
+};
+
+TensorLayout tensor_layout(int order, const int64_t* dims, int split, int L) {
+  TensorLayout t{};
+  t.M = 1;
+  t.J = 1;
+  for (int n = 0; n < split; ++n) t.M *= dims[n];
+  for (int n = split; n < order; ++n) t.J *= dims[n];
+  t.Mp = align_up(t.M, BM);
+  t.Jp = align_up(t.J, BK);
+  t.nmb = t.Mp / BM;
+  t.njb = t.Jp / BK;
+  t.L = L;
+  // [int32 row exponents][uint64 row maxima (slicing scratch)][blocked digit planes]
+  t.rmax_off = size_t(align_up(t.Mp * int64_t(sizeof(int)), 1024));
+  t.plane_off = t.rmax_off + size_t(align_up(t.Mp * 8, 1024));
+  t.total = t.plane_off + size_t(L) * size_t(t.Mp) * size_t(t.Jp);
+  return t;
+}
+
+// ---------------------------------------------------------------- digits --
+// Balanced base-256 digits of q = round(v * 2^(8L-2-e)), |v| < 2^e: d[0] in
+// [-65, 65], d[1..L-1] in [-128, 127], q = sum_s d[s] 256^(L-1-s).  The low three
+// digits come from the low 24 bits of q, the rest from the high part plus carry,
+// all in 32-bit integer arithmetic.
+template <int L>
+__device__ __forceinline__ void to_digits(double v, int e, int (&d)[L]) {
+  const int k = 8 * L - 2 - e;
+  const double scaled = (k >= -1022 && k <= 1023) ? v * __longlong_as_double((long long)(k + 1023) << 52)
+                                                  : scalbn(v, k);
+  const long long q = __double2ll_rn(scaled);   // |q| <= 2^(8L-2) <= 2^54
+  int x = int(uint32_t(q) & 0xFFFFFFu);
+#pragma unroll
+  for (int s = L - 1; s >= L - 3; --s) {
+    const int dd = ((x + 128) & 255) - 128;
+    d[s] = dd;
+    x = (x - dd) >> 8;
+  }
+  int y = int(q >> 24) + x;   // x = carry out of the low 24 bits (0 or 1)
+#pragma unroll
+  for (int s = L - 4; s >= 1; --s) {
+    const int dd = ((y + 128) & 255) - 128;
+    d[s] = dd;
+    y = (y - dd) >> 8;
+  }
+  d[0] = y;
+}
+
+// frexp exponent of a nonnegative double given by its bits (0 for zero)
+__device__ __forceinline__ int exp_of_bits(unsigned long long bits) {
+  const int field = int((bits >> 52) & 0x7FFu);
+  if (field != 0) return field - 1022;
+  int e = 0;
+  if (bits != 0ull) frexp(__longlong_as_double((long long)bits), &e);
+  return e;
+}
+
+// v * 2^e, exact (a power-of-two multiply) unless the result leaves the normal range
+__device__ __forceinline__ double times_pow2(double v, int e) {
+  return (e >= -1022 && e <= 1023) ? v * __longlong_as_double((long long)(e + 1023) << 52) : scalbn(v, e);
+}
+
+// ------------------------------------------------------ tensor slicing --
+__global__ void slice_rowmax_kernel(const double* __restrict__ x, int64_t M, int64_t J, int64_t jper,
+                                    unsigned long long* __restrict__ rmax) {
+  const int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int64_t j0 = int64_t(blockIdx.y) * jper;
+  const int64_t j1 = min(J, j0 + jper);
+  const double* p = x + m;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int64_t j = j0;
+  for (; j + 4 <= j1; j += 4) {
+    v0 = fmax(v0, fabs(__ldg(p + (j + 0) * M)));
+    v1 = fmax(v1, fabs(__ldg(p + (j + 1) * M)));
+    v2 = fmax(v2, fabs(__ldg(p + (j + 2) * M)));
+    v3 = fmax(v3, fabs(__ldg(p + (j + 3) * M)));
+  }
+  for (; j < j1; ++j) v0 = fmax(v0, fabs(__ldg(p + j * M)));
+  const double v = fmax(fmax(v0, v1), fmax(v2, v3));
+  atomicMax(rmax + m, (unsigned long long)__double_as_longlong(v));
+}
+
+// Thread: 16 consecutive rows m at every column j of its range (padding rows /
+// columns written as zeros); 16 bytes per plane into the blocked layout.
+template <int L, bool VEC>
+__global__ void __launch_bounds__(256) slice_planes_kernel(const double* __restrict__ x, int64_t M, int64_t J,
+                                                           int64_t Mp, int64_t Jp, int64_t njb, int64_t jper,
+                                                           const unsigned long long* __restrict__ rmax,
+                                                           int* __restrict__ rowexp, int8_t* __restrict__ planes) {
+  const int64_t m0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
+  if (m0 >= Mp) return;
+  int ex[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ex[i] = (m0 + i < M) ? exp_of_bits(rmax[m0 + i]) : 0;
+  if (blockIdx.y == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rowexp[m0 + i] = ex[i];
+  }
+  const int64_t mb = m0 / BM;
+  const int64_t j0 = int64_t(blockIdx.y) * jper;
+  const int64_t j1 = min(Jp, j0 + jper);
+  for (int64_t j = j0; j < j1; ++j) {
+    double v[16];
+    const double* src = x + M * j + m0;
+    if (j >= J) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0;
+    } else if (VEC && m0 + 16 <= M) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(src) + i);
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
+    }
+    uint32_t w[L][4];
+#pragma unroll
+    for (int s = 0; s < L; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[s][q] = 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      int d[L];
+      to_digits<L>(v[i], ex[i], d);
+#pragma unroll
+      for (int s = 0; s < L; ++s) w[s][i / 4] |= (uint32_t(d[s]) & 0xFFu) << (8 * (i % 4));
+    }
+    int8_t* blk = planes + ((mb * njb + j / BK) * L) * int64_t(TILE) + (j % BK) * BM + (m0 % BM);
+#pragma unroll
+    for (int s = 0; s < L; ++s)
+      *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
+// ------------------------------------------------------ factor slicing --
+// B[k, r] = KRP(factors)[k, r] (first factor fastest, tensor_ops.py:121-137),
+// times 2^rowexp[k] for the right side.
+struct BSpec {
+  const double* ptr[kMaxOrder];
+  int64_t dim[kMaxOrder];
+  int n;
+  const int* rowexp;  // nullable
+  int64_t K, Kp, Kc;  // Kp: K rounded up to whole 128-deep k blocks
+  int R, RP;
+};
+
+constexpr int EXP_NONE = int(0x80808080);   // memset(0x80) sentinel: column chunk has no nonzero
+
+// frexp exponent of |v| * 2^add (EXP_NONE for zero), without the multiply
+__device__ __forceinline__ int exp_of(double v, int add) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7FFFFFFFFFFFFFFFull;
+  if (bits == 0ull) return EXP_NONE;
+  return exp_of_bits(bits) + add;
+}
+
+// B preparation works on whole 128-deep k blocks (one GEMM B stage each): block
+// = 8 warps x 16 rows, lane = column (coalesced factor-row loads), H = column
+// halves (R <= 32: 1, else 2).  NF = number of Khatri-Rao factors when 1..3: the
+// warp's first row is decomposed into factor rows once and later rows advance a
+// mixed-radix cursor (no divisions; all 16 rows' loads in flight); NF = 0: any
+// count, one decomposition per row.
+template <int NF, int H>
+__device__ __forceinline__ void krp_rows16(const BSpec& s, int64_t k0, int lane, double (&v)[16][H],
+                                           int (&add)[16]) {
+  if constexpr (NF > 0) {
+    uint32_t dig[NF];
+    int64_t q = k0 < s.K ? k0 : 0;
+#pragma unroll
+    for (int f = 0; f < NF - 1; ++f) {
+      dig[f] = uint32_t(q % s.dim[f]);
+      q /= s.dim[f];
+    }
+    dig[NF - 1] = uint32_t(q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t k = k0 + i;
+      const bool in = k < s.K;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int r = lane + 32 * h;
+        double p = 1.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) p *= (in && r < s.R) ? __ldg(s.ptr[f] + size_t(dig[f]) * s.R + r) : 0.0;
+        v[i][h] = p;
+      }
+      add[i] = (s.rowexp && in) ? __ldg(s.rowexp + k) : 0;
+      // advance the cursor (first factor fastest)
+      ++dig[0];
+#pragma unroll
+      for (int f = 0; f < NF - 1; ++f) {
+        const bool wrap = dig[f] == uint32_t(s.dim[f]);
+        dig[f] = wrap ? 0u : dig[f];
+        dig[f + 1] += wrap ? 1u : 0u;
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+      const int64_t k = k0 + i;
+      const bool in = k < s.K;
+      int64_t q = in ? k : 0;
+      double p[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) p[h] = 1.0;
+#pragma unroll 1
+      for (int f = 0; f < s.n; ++f) {
+        int64_t idx = q;
+        if (f < s.n - 1) {
+          idx = q % s.dim[f];
+          q /= s.dim[f];
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int r = lane + 32 * h;
+          p[h] *= (in && r < s.R) ? __ldg(s.ptr[f] + idx * s.R + r) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h) v[i][h] = p[h];
+      add[i] = (s.rowexp && in) ? __ldg(s.rowexp + k) : 0;
+    }
+  }
+}
+
+// bexp[chunk][r] = max over the chunk's rows of the frexp exponent of |B[k, r]|
+// (B = KRP times 2^rowexp[k]); one atomic per k block and column.
+template <int NF, int H>
+__global__ void __launch_bounds__(256) bslice_exp_kernel(BSpec s, int* __restrict__ bexp) {
+  __shared__ int red[8][kMaxRank];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t kb0 = int64_t(blockIdx.x) * BK;
+  double v[16][H];
+  int add[16];
+  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, add);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int mx = EXP_NONE;
+    if (h < H) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) mx = max(mx, exp_of(v[i][h < H ? h : 0], add[i]));
+    }
+    red[warp][lane + 32 * h] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x < s.R) {
+    int m = red[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = max(m, red[w][threadIdx.x]);
+    if (m != EXP_NONE) atomicMax(bexp + (kb0 / s.Kc) * s.RP + threadIdx.x, m);
+  }
+}
+
+// Digits of one k block into shared memory (rows (t, r) of 128 digits, word
+// pitch 33 so the 32 lanes' stores hit distinct banks), then one contiguous
+// coalesced store of the block in the stage layout [t][r][k % 128].
+template <int L, int NF, int H>
+__global__ void __launch_bounds__(256) bslice_digits_kernel(BSpec s, const int* __restrict__ bexp,
+                                                            int8_t* __restrict__ bs) {
+  extern __shared__ __align__(16) uint32_t tile[];   // L * RP rows x 33 words
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t kb0 = int64_t(blockIdx.x) * BK;
+  const int64_t chunk = kb0 / s.Kc;
+  int e[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const int r = lane + 32 * h;
+    e[h] = r < s.R ? bexp[chunk * s.RP + r] : EXP_NONE;
+  }
+  double v[16][H];
+  int add[16];
+  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, add);
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const int r = lane + 32 * h;
+    if (r >= s.RP) continue;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint32_t w[L];
+#pragma unroll
+      for (int t = 0; t < L; ++t) w[t] = 0u;
+      if (e[h] != EXP_NONE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int d[L];
+          to_digits<L>(v[4 * g + i][h], e[h] - add[4 * g + i], d);   // (v 2^add) / 2^e
+#pragma unroll
+          for (int t = 0; t < L; ++t) w[t] |= (uint32_t(d[t]) & 0xFFu) << (8 * i);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < L; ++t) tile[(t * s.RP + r) * 33 + warp * 4 + g] = w[t];
+    }
+  }
+  __syncthreads();
+  const int nwords = L * s.RP * (BK / 4);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(bs + (kb0 / BK) * int64_t(L) * s.RP * BK);
+  for (int q = threadIdx.x; q < nwords; q += blockDim.x) dst[q] = tile[(q >> 5) * 33 + (q & 31)];
+}
+
+template <int L, int NF, int H>
+int launch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    NNCP_CUDA_TRY(cudaFuncSetAttribute(bslice_digits_kernel<L, NF, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(L * kMaxRank * 33 * 4)));
+    attr = true;
+  }
+  bslice_exp_kernel<NF, H><<<kblocks, 256, 0, st>>>(b, bexp);
+  NNCP_LAUNCH_CHECK();
+  bslice_digits_kernel<L, NF, H><<<kblocks, 256, size_t(L) * b.RP * 33 * 4, st>>>(b, bexp, bs);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+template <int L, int NF>
+int launch_bslice_h(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaStream_t st) {
+  // the cursor path needs dims below 2^32 (always: factor rows are int32-indexed)
+  return b.RP <= 32 ? launch_bslice<L, NF, 1>(b, bexp, bs, kblocks, st)
+                    : launch_bslice<L, NF, 2>(b, bexp, bs, kblocks, st);
+}
+
+template <int L>
+int dispatch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaStream_t st) {
+  switch (b.n) {
+    case 1: return launch_bslice_h<L, 1>(b, bexp, bs, kblocks, st);
+    case 2: return launch_bslice_h<L, 2>(b, bexp, bs, kblocks, st);
+    case 3: return launch_bslice_h<L, 3>(b, bexp, bs, kblocks, st);
+    default: return launch_bslice_h<L, 0>(b, bexp, bs, kblocks, st);
+  }
+}
+
+__global__ void group_reduce_kernel(const double* __restrict__ part, int groups, int64_t stride, int64_t n,
+                                    double* __restrict__ out) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    double s = part[e];
+    for (int g = 1; g < groups; ++g) s += part[int64_t(g) * stride + e];
+    out[e] = s;
+  }
+}
+
+// ------------------------------------------------------------- UMMA PTX --
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFFu);
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;                 // descriptor version (sm_100)
+  d |= uint64_t(layout) << 61;            // 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ uint32_t idesc_s8(int N, bool a_mn_major) {
+  return (2u << 4)                          // D: s32
+         | (1u << 7) | (1u << 10)           // A, B: signed 8-bit
+         | (uint32_t(a_mn_major) << 15)     // A major (B is K-major)
+         | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_s8(uint32_t dtmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+// --------------------------------------------------------------- GEMM ---
+template <int RP, int L>
+struct GemmCfg {
+  static constexpr int A_STAGE = TILE;                  // one digit-plane tile
+  static constexpr int B_STAGE = L * RP * BK;           // all B digit rows of one k block
+  static constexpr int NB = 2;
+  static constexpr int NA_FIT = (MAX_SMEM - 1024 - NB * B_STAGE) / A_STAGE;
+  static constexpr int NA = NA_FIT > 12 ? 12 : NA_FIT;
+  static constexpr int ACC = L * RP;                    // TMEM columns of one accumulator set
+  static constexpr int NBUF = (2 * ACC <= 512) ? 2 : 1;
+  static constexpr int NEED = NBUF * ACC;
+  static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = size_t(NB) * B_STAGE + size_t(NA) * A_STAGE + 1024;
+  static_assert(NA >= L, "one k block of digit tiles must fit in shared memory");
+  static_assert(ACC <= 512, "accumulator does not fit in TMEM");
+  static_assert(B_STAGE % 1024 == 0, "stages must keep 1 KB alignment");
+};
+
+struct GemmArgs {
+  int64_t rows;        // output rows: M (left) or J (right)
+  int64_t nkb;         // 128-deep k blocks of the (padded) contraction
+  int64_t kbc;         // k blocks per chunk
+  int64_t nchunks;
+  int64_t row_tiles;
+  int64_t items;       // row_tiles * groups
+  int groups;
+  const int* rowexp;   // left: per output row exponent; right: nullptr (folded into B)
+  const int* bexp;     // [nchunks][RP] frexp exponents of the column-chunk maxima of |B|
+  double* out;         // [group][r][row]
+  int64_t group_stride;
+  int R;
+};
+
+template <int SIDE, int RP, int L>
+__global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                                const __grid_constant__ CUtensorMap mapB,
+                                                                GemmArgs a) {
+  using C = GemmCfg<RP, L>;
+  constexpr bool LEFT = SIDE == NNCP_SIDE_LEFT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_b = smem;
+  uint8_t* smem_a = smem + C::NB * C::B_STAGE;
+  __shared__ __align__(8) uint64_t afull[C::NA], aempty[C::NA], bfull[C::NB], bempty[C::NB];
+  __shared__ __align__(8) uint64_t tfull[C::NBUF], tempty[C::NBUF];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NA; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < C::NB; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < C::NBUF; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tma_desc(&mapA);
+    prefetch_tma_desc(&mapB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "n"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer ----
+      int as = 0, bsx = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
+        const int64_t tile = it % a.row_tiles, g = it / a.row_tiles;
+        const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
+        for (int64_t kb = c0 * a.kbc, kend = min(a.nkb, c1 * a.kbc); kb < kend; ++kb) {
+          mbar_wait(&bempty[bsx], bph ^ 1u);
+          mbar_arrive_expect_tx(&bfull[bsx], C::B_STAGE);
+          tma_load_4d(smem_b + size_t(bsx) * C::B_STAGE, &mapB, &bfull[bsx], 0, 0, 0, int(kb));
+          if (++bsx == C::NB) {
+            bsx = 0;
+            bph ^= 1u;
+          }
+          const int mb = int(LEFT ? tile : kb), jb = int(LEFT ? kb : tile);
+#pragma unroll 1
+          for (int s = 0; s < L; ++s) {
+            mbar_wait(&aempty[as], aph ^ 1u);
+            mbar_arrive_expect_tx(&afull[as], C::A_STAGE);
+            tma_load_5d(smem_a + size_t(as) * C::A_STAGE, &mapA, &afull[as], 0, 0, s, jb, mb);
+            if (++as == C::NA) {
+              as = 0;
+              aph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer ------
+      int as = 0, bsx = 0, abuf = 0;
+      uint32_t aph = 0, bph = 0, tph = 0;
+      for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
+        const int64_t g = it / a.row_tiles;
+        const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
+        for (int64_t c = c0; c < c1; ++c) {
+          mbar_wait(&tempty[abuf], tph ^ 1u);
+          tc_fence_after();
+          const uint32_t dcol = tbase + uint32_t(abuf * C::ACC);
+          bool first = true;
+          for (int64_t kb = c * a.kbc, kend = min(a.nkb, (c + 1) * a.kbc); kb < kend; ++kb) {
+            mbar_wait(&bfull[bsx], bph);
+            tc_fence_after();
+            const uint32_t sb = smem_u32(smem_b + size_t(bsx) * C::B_STAGE);
+#pragma unroll 1
+            for (int s = 0; s < L; ++s) {
+              mbar_wait(&afull[as], aph);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(smem_a + size_t(as) * C::A_STAGE);
+              const int ntot = (L - s) * RP;
+#pragma unroll
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                // left: MN-major SW128 (32 k rows of 128 B per MMA); right: K-major SW128 (32 B per MMA)
+                const uint64_t da = LEFT ? smem_desc(sa + kk * 32 * 128, 1024, 2) : smem_desc(sa + kk * 32, 1024, 2);
+#pragma unroll 1
+                for (int n0 = 0; n0 < ntot; n0 += 256) {
+                  const int nn = ntot - n0 < 256 ? ntot - n0 : 256;
+                  const uint64_t db = smem_desc(sb + kk * 32 + (n0 / 8) * 1024, 1024, 2);
+                  umma_s8(dcol + uint32_t(s * RP + n0), da, db, idesc_s8(nn, LEFT),
+                          (first && s == 0 && kk == 0) ? 0u : 1u);
+                }
+              }
+              umma_commit(&aempty[as]);
+              if (++as == C::NA) {
+                as = 0;
+                aph ^= 1u;
+              }
+            }
+            first = false;
+            umma_commit(&bempty[bsx]);
+            if (++bsx == C::NB) {
+              bsx = 0;
+              bph ^= 1u;
+            }
+          }
+          umma_commit(&tfull[abuf]);
+          if (++abuf == C::NBUF) {
+            abuf = 0;
+            tph ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue --------
+    const int quad = warp & 3;
+    int abuf = 0;
+    uint32_t tph = 0;
+    for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
+      const int64_t tile = it % a.row_tiles, g = it / a.row_tiles;
+      const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
+      const int64_t row = tile * BM + quad * 32 + lane;
+      const bool valid = row < a.rows;
+      const int ex = (a.rowexp != nullptr && valid) ? a.rowexp[row] : 0;
+      double acc[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+      for (int64_t c = c0; c < c1; ++c) {
+        mbar_wait(&tfull[abuf], tph);
+        tc_fence_after();
+        const uint32_t taddr = tbase + uint32_t(abuf * C::ACC) + (uint32_t(quad * 32) << 16);
+        int eb[RP];   // column-chunk exponents, with the 2^-12 of the two digit scales
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const int e = __ldg(a.bexp + c * RP + r);
+          eb[r] = (e == EXP_NONE ? 0 : e) - 12;   // an all-zero column chunk accumulated zeros
+        }
+#pragma unroll
+        for (int rg = 0; rg < RP / 8; ++rg) {
+          uint32_t v[L][8];
+#pragma unroll
+          for (int l = 0; l < L; ++l) tmem_ld8(taddr + uint32_t(l * RP + rg * 8), v[l]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            double s = double(int(v[L - 1][i]));
+#pragma unroll
+            for (int l = L - 2; l >= 0; --l) s = fma(s, 0.00390625, double(int(v[l][i])));
+            acc[rg * 8 + i] += times_pow2(s, ex + eb[rg * 8 + i]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[abuf]);
+        if (++abuf == C::NBUF) {
+          abuf = 0;
+          tph ^= 1u;
+        }
+      }
+      if (valid) {
+        double* o = a.out + g * a.group_stride + row;
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if (r < a.R) o[int64_t(r) * a.rows] = acc[r];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS));
+  }
+}
+
+// ------------------------------------------------------------- host side --
+int encode_u8(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+              const cuuint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(NNCP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, cuuint32_t(rank), const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NNCP_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string(int(r)));
+  return NNCP_OK;
+}
+
+struct CallPlan {
+  TensorLayout t;
+  int RP;
+  int64_t K, Kp, Kc, nchunks, rows, row_tiles;
+  int groups;
+  size_t bexp_off, bs_off, part_off, ws_bytes;
+};
+
+CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank, int L) {
+  CallPlan p{};
+  p.t = tensor_layout(order, dims, split, L);
+  p.RP = int(align_up(rank, 16));
+  const bool left = side == NNCP_SIDE_LEFT;
+  p.K = left ? p.t.J : p.t.M;
+  p.Kp = left ? p.t.Jp : p.t.Mp;
+  p.rows = left ? p.t.M : p.t.J;
+  p.row_tiles = left ? p.t.nmb : p.t.njb;
+  const int64_t sms = num_sms();
+  if (left) {
+    p.groups = 1;
+    p.Kc = std::min<int64_t>(KC_MAX, align_up(p.Kp, 256));
+  } else {
+    // split the contraction into groups so row_tiles x groups fills the SMs; the
+    // row tiles of a group stream the same B chunks at the same time (L2 reuse)
+    const int64_t want = std::max<int64_t>(1, sms / p.row_tiles);
+    p.Kc = std::min<int64_t>(KC_MAX, std::max<int64_t>(256, align_up((p.Kp + want - 1) / want, 256)));
+    const int64_t nch = (p.Kp + p.Kc - 1) / p.Kc;
+    p.groups = int(std::min<int64_t>(want, nch));
+  }
+  p.nchunks = (p.Kp + p.Kc - 1) / p.Kc;
+  p.bexp_off = 0;
+  p.bs_off = size_t(align_up(p.nchunks * p.RP * 4, 1024));
+  p.part_off = p.bs_off + size_t(align_up(int64_t(L) * p.RP * p.Kp, 1024));
+  p.ws_bytes = p.part_off + (p.groups > 1 ? size_t(p.groups) * p.rows * rank * sizeof(double) : 0);
+  return p;
+}
+
+template <int SIDE, int RP, int L>
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& ga, cudaStream_t st) {
+  using C = GemmCfg<RP, L>;
+  static bool attr = false;
+  if (!attr) {
+    NNCP_CUDA_TRY(cudaFuncSetAttribute(sliced_gemm_kernel<SIDE, RP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(C::SMEM)));
+    attr = true;
+  }
+  const unsigned ctas = unsigned(std::min<int64_t>(ga.items, num_sms()));
+  sliced_gemm_kernel<SIDE, RP, L><<<ctas, THREADS, C::SMEM, st>>>(ma, mb, ga);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+template <int L>
+int dispatch_gemm(int side, int rp, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& ga,
+                  cudaStream_t st) {
+#define NNCP_SLICED_CASE(RPV)                                                   \
+  case RPV:                                                                     \
+    return side == NNCP_SIDE_LEFT ? launch_gemm<NNCP_SIDE_LEFT, RPV, L>(ma, mb, ga, st) \
+                                  : launch_gemm<NNCP_SIDE_RIGHT, RPV, L>(ma, mb, ga, st);
+  switch (rp) {
+    NNCP_SLICED_CASE(16)
+    NNCP_SLICED_CASE(32)
+    NNCP_SLICED_CASE(48)
+    NNCP_SLICED_CASE(64)
+    default:
+      return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP: rank above NNCP_MAX_RANK");
+  }
+#undef NNCP_SLICED_CASE
+}
+
+int check_levels(int L) {
+  if (L != 6 && L != 7) return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP supports 6 or 7 digit levels");
+  return NNCP_OK;
+}
+
+}  // namespace sliced
+
+// ---------------------------------------------------------- entry points --
+size_t sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels) {
+  return sliced::tensor_layout(order, dims, split, levels).total;
+}
+
+size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int levels) {
+  const auto l = sliced::plan_call(order, dims, split, NNCP_SIDE_LEFT, rank, levels);
+  const auto r = sliced::plan_call(order, dims, split, NNCP_SIDE_RIGHT, rank, levels);
+  return std::max(l.ws_bytes, r.ws_bytes);
+}
+
+int slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* out, size_t bytes,
+                 cudaStream_t st) {
+  using namespace sliced;
+  if (int rc = check_levels(levels)) return rc;
+  const TensorLayout t = tensor_layout(order, dims, split, levels);
+  if (bytes < t.total) return fail(NNCP_ERR_VALUE, "sliced tensor buffer too small");
+  if (reinterpret_cast<uintptr_t>(out) % 1024) return fail(NNCP_ERR_VALUE, "sliced tensor buffer must be 1 KB aligned");
+  if (t.nmb >= (int64_t(1) << 31) || t.njb >= (int64_t(1) << 31))
+    return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP: unfolding dimension too large");
+  uint8_t* base = static_cast<uint8_t*>(out);
+  int* rowexp = reinterpret_cast<int*>(base);
+  int8_t* planes = reinterpret_cast<int8_t*>(base + t.plane_off);
+  unsigned long long* rmax = reinterpret_cast<unsigned long long*>(base + t.rmax_off);
+  NNCP_CUDA_TRY(cudaMemsetAsync(rmax, 0, size_t(t.Mp) * 8, st));
+  const int64_t target = int64_t(num_sms()) * 16;
+  const int64_t mblocks = (t.M + 255) / 256;
+  int64_t jsplit = std::max<int64_t>(1, std::min<int64_t>(t.J, (target + mblocks - 1) / mblocks));
+  int64_t jper = (t.J + jsplit - 1) / jsplit;
+  jsplit = (t.J + jper - 1) / jper;
+  slice_rowmax_kernel<<<dim3(unsigned(mblocks), unsigned(jsplit)), 256, 0, st>>>(x, t.M, t.J, jper, rmax);
+  NNCP_LAUNCH_CHECK();
+  const int64_t gblocks = (t.Mp / 16 + 255) / 256;
+  int64_t js2 = std::max<int64_t>(1, std::min<int64_t>(t.Jp, (target + gblocks - 1) / gblocks));
+  int64_t jper2 = (t.Jp + js2 - 1) / js2;
+  js2 = (t.Jp + jper2 - 1) / jper2;
+  const dim3 grid{unsigned(gblocks), unsigned(js2), 1u};
+  const bool vec = (t.M % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+#define NNCP_SLICE_LAUNCH(LV, V) \
+  slice_planes_kernel<LV, V><<<grid, 256, 0, st>>>(x, t.M, t.J, t.Mp, t.Jp, t.njb, jper2, rmax, rowexp, planes)
+  if (levels == 6) {
+    if (vec) NNCP_SLICE_LAUNCH(6, true); else NNCP_SLICE_LAUNCH(6, false);
+  } else {
+    if (vec) NNCP_SLICE_LAUNCH(7, true); else NNCP_SLICE_LAUNCH(7, false);
+  }
+#undef NNCP_SLICE_LAUNCH
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, int split, int side,
+                          const double* const* factors, int rank, int levels, double* out, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
+  using namespace sliced;
+  if (int rc = check_levels(levels)) return rc;
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP: rank outside [1, 64]");
+  const CallPlan p = plan_call(order, dims, split, side, rank, levels);
+  if (ws == nullptr || ws_bytes < p.ws_bytes) return fail(NNCP_ERR_VALUE, "workspace too small for sliced MTTKRP");
+  if (reinterpret_cast<uintptr_t>(ws) % 1024) return fail(NNCP_ERR_VALUE, "workspace must be 1 KB aligned");
+  const bool left = side == NNCP_SIDE_LEFT;
+  const uint8_t* base = static_cast<const uint8_t*>(sliced_x);
+  const int* rowexp = reinterpret_cast<const int*>(base);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* bexp = reinterpret_cast<int*>(w + p.bexp_off);
+  int8_t* bs = reinterpret_cast<int8_t*>(w + p.bs_off);
+
+  BSpec b{};
+  if (left) {
+    b.n = order - split;
+    for (int f = 0; f < b.n; ++f) {
+      b.ptr[f] = factors[split + f];
+      b.dim[f] = dims[split + f];
+    }
+    b.rowexp = nullptr;
+  } else {
+    b.n = split;
+    for (int f = 0; f < b.n; ++f) {
+      b.ptr[f] = factors[f];
+      b.dim[f] = dims[f];
+    }
+    b.rowexp = rowexp;
+  }
+  for (int f = 0; f < b.n; ++f)
+    if (!b.ptr[f]) return fail(NNCP_ERR_VALUE, "null factor pointer on the contracted side");
+  b.K = p.K;
+  b.Kp = p.Kp;
+  b.Kc = p.Kc;
+  b.R = rank;
+  b.RP = p.RP;
+  NNCP_CUDA_TRY(cudaMemsetAsync(bexp, 0x80, size_t(p.nchunks) * p.RP * 4, st));   // EXP_NONE
+  const unsigned kblocks = unsigned(p.Kp / BK);
+  if (int rc = levels == 6 ? dispatch_bslice<6>(b, bexp, bs, kblocks, st) : dispatch_bslice<7>(b, bexp, bs, kblocks, st))
+    return rc;
+
+  // A: blocked digit planes as a 5-D tensor {m % 128, j % 128, plane, jb, mb}
+  CUtensorMap ma, mb;
+  {
+    const cuuint64_t d[5] = {BM, BK, cuuint64_t(levels), cuuint64_t(p.t.njb), cuuint64_t(p.t.nmb)};
+    const cuuint64_t s[4] = {BM, TILE, cuuint64_t(levels) * TILE, cuuint64_t(p.t.njb) * levels * TILE};
+    const cuuint32_t box[5] = {BM, BK, 1, 1, 1};
+    if (int rc = encode_u8(&ma, base + p.t.plane_off, 5, d, s, box)) return rc;
+  }
+  // B: blocked digit rows as a 4-D tensor {k % 128, r, digit, kb}
+  {
+    const cuuint64_t d[4] = {BK, cuuint64_t(p.RP), cuuint64_t(levels), cuuint64_t(p.Kp / BK)};
+    const cuuint64_t s[3] = {BK, cuuint64_t(p.RP) * BK, cuuint64_t(levels) * p.RP * BK};
+    const cuuint32_t box[4] = {BK, cuuint32_t(p.RP), cuuint32_t(levels), 1};
+    if (int rc = encode_u8(&mb, bs, 4, d, s, box)) return rc;
+  }
+
+  GemmArgs ga{};
+  ga.rows = p.rows;
+  ga.nkb = p.Kp / BK;
+  ga.kbc = p.Kc / BK;
+  ga.nchunks = p.nchunks;
+  ga.row_tiles = p.row_tiles;
+  ga.groups = p.groups;
+  ga.items = p.row_tiles * p.groups;
+  ga.rowexp = left ? rowexp : nullptr;
+  ga.bexp = bexp;
+  ga.out = p.groups > 1 ? reinterpret_cast<double*>(w + p.part_off) : out;
+  ga.group_stride = p.rows * rank;
+  ga.R = rank;
+  int rc = levels == 6 ? dispatch_gemm<6>(side, p.RP, ma, mb, ga, st) : dispatch_gemm<7>(side, p.RP, ma, mb, ga, st);
+  if (rc) return rc;
+  if (p.groups > 1) {
+    const int64_t n = p.rows * rank;
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    group_reduce_kernel<<<blocks, 256, 0, st>>>(ga.out, p.groups, n, n, out);
+    NNCP_LAUNCH_CHECK();
+  }
+  return NNCP_OK;
+}
+
+}  // namespace nncp

@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dimtree import DimTreeContext, DimTreePlan
+from .dimtree import DimTreeContext, DimTreePlan, SlicedTensor
 from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, RankLayout, ThreadCollectives,
                    ThreadGrid, block_partition)
 from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
@@ -67,6 +67,9 @@ class RunConfig:
     strict_split: bool = False
     initial_factors: FactorSet = None
     cuda_graph: bool = None   # None = auto: replay the sweep as a CUDA graph when it is capturable
+    # partial-MTTKRP engine: "sliced" = int8 tensor cores over a once-sliced tensor
+    # (DESIGN.md §4.4), "fp64" = FP64 DMMA, "auto" = sliced when the slices fit in HBM
+    mttkrp_kernel: str = "auto"
 
     def validate(self, order: int):
         if self.rank < 1:
@@ -85,6 +88,8 @@ class RunConfig:
             raise NotImplementedError(
                 f"algorithm {self.algorithm!r} is outside this build's hot-path scope "
                 f"(supported: {', '.join(IN_SCOPE_ALGORITHMS)})")
+        if self.mttkrp_kernel not in ("auto", "sliced", "fp64"):
+            raise ValueError(f"unknown mttkrp_kernel {self.mttkrp_kernel!r} (auto, sliced, fp64)")
         if self.rank > _lib.MAX_RANK:
             raise NotImplementedError(f"rank {self.rank} exceeds the device limit {_lib.MAX_RANK}")
         if order > _lib.MAX_ORDER:
@@ -225,6 +230,22 @@ class _EventTimer:
 
 # ------------------------------------------------------------ engine --------
 
+SLICED_MIN_ELEMS = 1 << 22       # below this the fp64 path's fewer launches win
+SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
+
+
+def _use_sliced(kind: str, dims, split: int, dev) -> bool:
+    """Resolve RunConfig.mttkrp_kernel for one execution context."""
+    if kind == "fp64":
+        return False
+    if kind == "sliced":
+        return True
+    if int(np.prod(dims)) < SLICED_MIN_ELEMS:
+        return False
+    free, _ = torch.cuda.mem_get_info(dev)
+    return SlicedTensor.nbytes(dims, split) + SLICED_HBM_MARGIN <= free
+
+
 class _Engine:
     """One execution context (one GPU, or one simulated worker) of the SPMD program."""
 
@@ -251,8 +272,14 @@ class _Engine:
             self.owned_parts = list(layout.owned_parts)
         self.n_owned = [s.stop - s.start for s in self.owned_rows]
         self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
-        self.ws = Workspace(self.plan.workspace_bytes())
-        self.ctx = DimTreeContext(self.plan, workspace=self.ws)
+        self.sliced = None
+        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, dev):
+            self.sliced = SlicedTensor(x_local, self.dims, self.plan.split)
+        ws_bytes = self.plan.workspace_bytes()
+        if self.sliced is not None:
+            ws_bytes = max(ws_bytes, self.plan.sliced_workspace_bytes(self.sliced.levels))
+        self.ws = Workspace(ws_bytes)
+        self.ctx = DimTreeContext(self.plan, workspace=self.ws, sliced=self.sliced)
         f64 = dict(dtype=torch.float64, device=dev)
         R, N = self.R, self.N
         self.grams = torch.zeros((N, R, R), **f64)

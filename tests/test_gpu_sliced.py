@@ -1,0 +1,191 @@
+"""Sliced-tensor partial MTTKRP (int8 tensor cores, Ozaki-scheme digit planes;
+DESIGN.md §4.4) vs the reference's golden vectors, the CPU oracle and the FP64
+DMMA path.  Same tolerances as every other MTTKRP in the north star: <= 1e-12
+relative Frobenius for a single MTTKRP, error traces <= 1e-9 over the first
+10 iterations, final normalised factors <= 1e-6."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import nncp_oracle as O
+from tests.conftest import rel_fro
+
+pytestmark = pytest.mark.gpu
+
+MTTKRP_TOL = 1e-12
+TRACE_TOL = 1e-9
+FACTOR_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1909_01149_b200 as pkg
+
+    return pkg
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _sliced(P, x, plan, levels=6):
+    from paper_1909_01149_b200.dimtree import SlicedTensor
+
+    return SlicedTensor(x, plan.dims, plan.split, levels)
+
+
+@pytest.mark.parametrize("levels", [6, 7])
+def test_sliced_partials_vs_golden(P, golden, levels):
+    g = golden("mttkrp.npz")
+    for k in range(int(g["ncases"])):
+        dims = tuple(int(d) for d in g[f"c{k}_dims"])
+        r = int(g[f"c{k}_rank"])
+        x = P.DenseTensor(dims, g[f"c{k}_x"]).to_device()
+        hs = [g[f"c{k}_h{n}"] for n in range(len(dims))]
+        plan = P.DimTreePlan.create(dims, r)
+        sl = _sliced(P, x, plan, levels)
+        tl = P.partial_mttkrp(x, hs, "left", plan, sliced=sl)
+        tr = P.partial_mttkrp(x, hs, "right", plan, sliced=sl)
+        assert rel_fro(_np(tl.data), g[f"c{k}_tl"]) <= MTTKRP_TOL, (k, dims, r)
+        assert rel_fro(_np(tr.data), g[f"c{k}_tr"]) <= MTTKRP_TOL, (k, dims, r)
+
+
+@pytest.mark.parametrize("dims,r", [((128, 96, 80), 32), ((64, 48, 40, 24), 16), ((4096, 64, 32), 20),
+                                    ((100, 64, 64), 64), ((256, 256, 300), 8), ((7, 9, 11), 5),
+                                    ((96, 64, 48), 40), ((64, 64, 64, 8), 48), ((130, 70, 50), 56),
+                                    ((30, 20, 10, 8, 6), 12), ((2, 3, 4, 5, 6, 7), 3), ((33, 17, 5), 1),
+                                    ((257, 129, 65), 33)])
+def test_sliced_partials_vs_oracle(P, dims, r):
+    rng = np.random.default_rng(sum(dims) + r)
+    x = rng.random(int(np.prod(dims)))
+    hs = [rng.random((d, r)) for d in dims]
+    plan = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    sl = _sliced(P, xd, plan)
+    for side, fn in (("left", O.partial_left), ("right", O.partial_right)):
+        got = _np(P.partial_mttkrp(xd, hs, side, plan, sliced=sl).data)
+        want = fn(x, dims, plan.split, hs)
+        assert rel_fro(got, want) <= MTTKRP_TOL, side
+
+
+@pytest.mark.parametrize("dims,r", [((512, 512, 512), 16), ((180, 100, 17000), 32), ((64, 64, 64, 64), 64),
+                                    ((2048, 1024, 60), 20), ((1000, 1000, 999), 48)])
+def test_sliced_vs_fp64_path_multichunk(P, dims, r):
+    """Shapes with several contraction chunks (K > 16384 on the left, split-K groups on the right),
+    uneven tiles, R padded to 16/48/64: sliced == FP64 DMMA path (itself oracle-checked) to 1e-12."""
+    import torch
+
+    from paper_1909_01149_b200 import synth
+
+    fs = synth.truth_factors(dims, r, 7, "uniform")
+    x = synth.synthetic_block(dims, fs, 0.01, 7)
+    plan = P.DimTreePlan.create(dims, r)
+    rng = np.random.default_rng(r)
+    hs = [torch.from_numpy(rng.random((d, r))).cuda() for d in dims]
+    sl = _sliced(P, x, plan)
+    for side in ("left", "right"):
+        ref = P.partial_mttkrp(x, hs, side, plan).data
+        got = P.partial_mttkrp(x, hs, side, plan, sliced=sl).data
+        err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+        assert err <= MTTKRP_TOL, (side, err)
+    del sl, x
+    torch.cuda.empty_cache()
+
+
+def test_sliced_signed_and_wide_range(P):
+    """Mixed-sign tensors and factors, zeros, and per-row magnitudes over 2^40: the
+    row / column-chunk scales keep every row at full relative precision."""
+    dims, r = (300, 200, 150), 24
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(int(np.prod(dims)))
+    rows = np.prod(dims[:2])
+    x = x.reshape(dims[2], rows) * np.exp2(rng.integers(-20, 20, rows))[None, :]   # per-row scale (left side rows)
+    x[:, ::7] = 0.0
+    x = x.ravel()
+    hs = [rng.standard_normal((d, r)) for d in dims]
+    plan = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    sl = _sliced(P, xd, plan, 7)
+    got = _np(P.partial_mttkrp(xd, hs, "left", plan, sliced=sl).data)
+    want = O.partial_left(x, dims, plan.split, hs)
+    # mixed signs: the bound is relative to sum |x||b| (cancellation), checked per row
+    absref = O.partial_left(np.abs(x), dims, plan.split, [np.abs(h) for h in hs])
+    assert np.max(np.abs(got - want) / np.maximum(absref, 1e-300)) <= 1e-13
+    got = _np(P.partial_mttkrp(xd, hs, "right", plan, sliced=sl).data)
+    want = O.partial_right(x, dims, plan.split, hs)
+    absref = O.partial_right(np.abs(x), dims, plan.split, [np.abs(h) for h in hs])
+    assert np.max(np.abs(got - want) / np.maximum(absref, 1e-300)) <= 1e-13
+
+
+def test_sliced_bitwise_reproducible(P):
+    import torch
+
+    from paper_1909_01149_b200 import synth
+
+    dims, r = (640, 640, 320), 32
+    fs = synth.truth_factors(dims, r, 3, "uniform")
+    x = synth.synthetic_block(dims, fs, 0.01, 3)
+    plan = P.DimTreePlan.create(dims, r)
+    sl = _sliced(P, x, plan)
+    hs = [torch.from_numpy(f).cuda() for f in fs]
+    for side in ("left", "right"):
+        a = P.partial_mttkrp(x, hs, side, plan, sliced=sl).data.clone()
+        b = P.partial_mttkrp(x, hs, side, plan, sliced=sl).data.clone()
+        assert torch.equal(a, b), side
+
+
+def test_sliced_runs_vs_golden(P, golden):
+    """Every golden sequential run (live reference traces) with the sliced engine forced."""
+    g = golden("runs.npz")
+    for name in [str(n) for n in g["names"]]:
+        dims = tuple(int(d) for d in g[f"{name}_dims"])
+        r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
+        algo = str(g[f"{name}_algo"])
+        x = P.DenseTensor(dims, g[f"{name}_x"])
+        cfg = P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed, mttkrp_kernel="sliced")
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            rep = P.nncp_sequential(x, cfg)
+        ref = g[f"{name}_errors"]
+        got = np.array(rep.errors)
+        k = min(11, len(ref))
+        tol = TRACE_TOL if algo != "nes" else 5e-8   # NES: documented discontinuities (test_gpu_stateful.py)
+        assert np.max(np.abs(got[:k] - ref[:k])) <= tol, (name, np.max(np.abs(got[:k] - ref[:k])))
+        if algo != "nes":
+            for n in range(len(dims)):
+                assert np.max(np.abs(rep.model.factors[n] - g[f"{name}_f{n}"])) <= FACTOR_TOL, (name, n)
+
+
+@pytest.mark.parametrize("dims,r,algo,iters", [((128, 128, 128), 16, "hals", 8), ((32, 32, 32, 32), 32, "bpp", 4),
+                                               ((256, 128, 16), 20, "hals", 6), ((96, 80, 64), 64, "mu", 5)])
+def test_sliced_runs_vs_oracle(P, dims, r, algo, iters):
+    rng = np.random.default_rng(sum(dims) * r)
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    x = x + 0.01 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))
+    errors, factors, lam, _, _ = O.run_sequential(x, dims, r, algo, iters, 0.0, 0)
+    rep = P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0,
+                                                                mttkrp_kernel="sliced"))
+    assert np.max(np.abs(np.array(rep.errors) - np.array(errors))) <= TRACE_TOL
+    for a, b in zip(rep.model.factors, factors):
+        assert np.max(np.abs(a - b)) <= FACTOR_TOL
+
+
+def test_sliced_graph_matches_eager(P):
+    rng = np.random.default_rng(11)
+    dims, r = (160, 144, 120), 24
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    runs = []
+    for graph in (False, True):
+        cfg = P.RunConfig(rank=r, algorithm="hals", max_iters=5, tol=0.0, cuda_graph=graph, mttkrp_kernel="sliced")
+        runs.append(P.nncp_sequential(P.DenseTensor(dims, x), cfg))
+    assert runs[0].errors == runs[1].errors
+    for a, b in zip(runs[0].model.factors, runs[1].model.factors):
+        assert np.array_equal(a, b)
