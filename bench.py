@@ -62,14 +62,6 @@ def load_peaks():
         return 6650.0, "fallback B200_PROFILING.md"
 
 
-def roofline_times(dims, rank, hbm_gbs):
-    """Per partial MTTKRP: max(bytes/BW, flops/P64)."""
-    size = math.prod(dims)
-    t_bytes = 8.0 * size / (hbm_gbs * 1e9)
-    t_flops = 2.0 * size * rank / (FP64_PEAK_TFLOPS * 1e12)
-    return t_bytes, t_flops
-
-
 # ------------------------------------------------------------ clocks --------
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
@@ -240,7 +232,8 @@ def gpu_run(args, conf):
     errors = list(eng.report.errors)
     out = dict(dev_s=dev_s, wall=wall, k_left=kl_sum / max(1, len(k_left)), k_right=kr_sum / max(1, len(k_right)),
                n_left=len(k_left), n_right=len(k_right), clocks=clk, launches=int(launches), errors=errors,
-               local_dims=layout.local_dims, grid=grid, world=world, rank=rank)
+               local_dims=layout.local_dims, grid=grid, world=world, rank=rank, split=eng.plan.split,
+               levels=eng.sliced.levels if eng.sliced is not None else None)
     # ------------------------------------------------------- e2e leg ----------
     del eng
     try:
@@ -298,7 +291,6 @@ def main():
     conf = CONFIGS[args.config]
     dims, R = conf["dims"], conf["rank"]
     hbm_gbs, hbm_src = load_peaks()
-    t_bytes, t_flops = roofline_times(dims, R, hbm_gbs)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     config = {"workload": f"{args.config}: {'x'.join(map(str, dims))} float64, rank {R}, {conf['algo'].upper()}, "
@@ -326,30 +318,51 @@ def main():
         return
     s_iter = res["dev_s"] / args.steps
     size = math.prod(dims)
-    dom = "left" if res["k_left"] >= res["k_right"] else "right"   # dominant (slower) partial kernel
+    dom = "left" if res["k_left"] >= res["k_right"] else "right"   # dominant (slower) partial MTTKRP
     k_dom = res["k_" + dom]
     mttkrp_s = res["k_left"] + res["k_right"]             # both partials of one sweep
-    mttkrp_tflops = 4.0 * size * R / mttkrp_s / 1e12 if mttkrp_s > 0 else None
-    t_roof_partial = max(t_bytes, t_flops) / res["world"]
-    bound = "tensor" if t_flops >= t_bytes else "hbm"
-    local_size = math.prod(res["local_dims"])
-    if bound == "tensor":
-        achieved = 2.0 * local_size * R / k_dom / 1e12
-        peak, unit, psrc = FP64_PEAK_TFLOPS, "TFLOP/s", FP64_PEAK_SRC
+    local = res["local_dims"]
+    local_size = math.prod(local)
+    # FP64-path roofline of the two partials: max(8 I / BW, 2 I R / P64) each
+    t_fp64_roof = 2 * max(8.0 * local_size / (hbm_gbs * 1e9), 2.0 * local_size * R / (FP64_PEAK_TFLOPS * 1e12))
+    L = res["levels"]
+    if L is not None:
+        # sliced engine: HBM-bound on the int8 digit planes
+        s_ = res["split"]
+        M, J = math.prod(local[:s_]), math.prod(local[s_:])
+        Mp, Jp, RP = -(-M // 128) * 128, -(-J // 128) * 128, -(-R // 16) * 16
+        planes = L * Mp * Jp
+        kp = Jp if dom == "left" else Mp
+        rows = M if dom == "left" else J
+        alg = planes + L * RP * kp + rows * R * 8     # digit planes + factor digits + fp64 output
+        achieved = alg / k_dom / 1e9
+        t_sliced_roof = 2 * planes / (hbm_gbs * 1e9)
+        roofline = {"kernel": f"sliced_gemm_kernel<{dom}> + factor-digit prep (tcgen05.mma kind::i8 over {L} int8 "
+                              "digit planes of the once-sliced tensor, TMA 16 KB tiles, TMEM int32 accumulators)",
+                    "bound": "hbm", "algorithmic": f"{alg:.4g} B per launch ({L} digit planes {planes:.4g} B + "
+                                                   f"factor digits + fp64 output)",
+                    "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
+                    "peak_source": hbm_src + " (of measured)"}
     else:
-        achieved = 8.0 * local_size / k_dom / 1e9
-        peak, unit, psrc = hbm_gbs, "GB/s", hbm_src
-    traffic = None
+        t_sliced_roof = None
+        bound = "tensor" if 2.0 * R / FP64_PEAK_TFLOPS / 1e12 >= 8.0 / hbm_gbs / 1e9 else "hbm"
+        if bound == "tensor":
+            achieved, peak, unit, psrc = 2.0 * local_size * R / k_dom / 1e12, FP64_PEAK_TFLOPS, "TFLOP/s", FP64_PEAK_SRC
+        else:
+            achieved, peak, unit, psrc = 8.0 * local_size / k_dom / 1e9, hbm_gbs, "GB/s", hbm_src
+        roofline = {"kernel": f"mttkrp_{dom}_tma (FP64 DMMA GEMM fed by TMA, KRP on the fly)", "bound": bound,
+                    "algorithmic": (f"{2 * local_size * R:.4g} flop" if bound == "tensor"
+                                    else f"{8 * local_size:.4g} B") + " per launch",
+                    "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak, "peak_source": psrc}
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    traffic = None
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
-    # ALS iteration roofline: two partials + TTV chain bytes (T_L read twice + written once)
-    ttv_bytes = 0
-    split = 2 if len(dims) == 3 else 2
-    lead = math.prod(dims[:split]) * R * 8
-    ttv_bytes += 3 * lead
-    t_roof_iter = (2 * max(t_bytes, t_flops) + ttv_bytes / (hbm_gbs * 1e9)) / res["world"]
+            tr = json.load(fh)
+        key = ("sliced_" if L is not None else "") + dom
+        traffic = tr.get(key, {}).get("dram_bytes_per_launch")
+    roofline["traffic"] = traffic
+    mttkrp_tflops = 4.0 * local_size * R / mttkrp_s / 1e12 if mttkrp_s > 0 else None
     cpu = None
     if res["world"] == 1 and not args.no_cpu_baseline:
         try:
@@ -361,15 +374,14 @@ def main():
         "metric": METRIC, "value": s_iter, "unit": "s/iter", "n_gpus": res["world"], "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": s_iter * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated in HBM)", "config": config,
+        "mttkrp_engine": f"sliced int8 tensor cores, {L} digit levels" if L is not None else "fp64 DMMA",
         "mttkrp_tflops": mttkrp_tflops,
-        "mttkrp_roofline_frac": (2 * t_roof_partial) / mttkrp_s if mttkrp_s > 0 else None,
-        "iter_roofline_frac": t_roof_iter / s_iter,
+        "mttkrp_tflops_note": "FP64-equivalent: 4 I R flop of the two partial MTTKRPs / their time",
+        "mttkrp_vs_fp64_roofline": t_fp64_roof / mttkrp_s if mttkrp_s > 0 else None,
+        "mttkrp_roofline_frac": (t_sliced_roof / mttkrp_s if t_sliced_roof else t_fp64_roof / mttkrp_s)
+        if mttkrp_s > 0 else None,
         "partial_ms": {"left": res["k_left"] * 1e3, "right": res["k_right"] * 1e3},
-        "roofline": {"kernel": f"mttkrp_{dom}_tma (dominant partial MTTKRP: TMA + DMMA GEMM, KRP on the fly)",
-                     "bound": bound, "algorithmic": (f"{2 * local_size * R:.4g} flop" if bound == "tensor"
-                                                     else f"{8 * local_size:.4g} B") + " per launch",
-                     "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                     "peak_source": psrc, "traffic": traffic},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": res["e2e_s"] / args.steps, "unit": "s/iter",
                 "h2d_bytes_per_step": res["h2d_bytes"] // args.steps,
