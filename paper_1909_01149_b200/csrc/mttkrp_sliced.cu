@@ -52,7 +52,7 @@ constexpr int BK = 128;                 // contraction elements (int8 bytes) per
 constexpr int TILE = BM * BK;           // bytes of one digit-plane tile (16 KB)
 constexpr int64_t KC_MAX = 16384;       // contraction chunk between int32 -> fp64 conversions
                                         // (multiple of 256; L * 2^14 * KC_MAX < 2^31 keeps int32 exact)
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;          // TMA warp, MMA warp, 8 epilogue warps
 constexpr int MAX_SMEM = 227 * 1024;
 
 __host__ __device__ constexpr int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -83,31 +83,56 @@ TensorLayout tensor_layout(int order, const int64_t* dims, int split, int L) {
 }
 
 // ---------------------------------------------------------------- digits --
-// Balanced base-256 digits of q = round(v * 2^(8L-2-e)), |v| < 2^e: d[0] in
-// [-65, 65], d[1..L-1] in [-128, 127], q = sum_s d[s] 256^(L-1-s).  The low three
-// digits come from the low 24 bits of q, the rest from the high part plus carry,
-// all in 32-bit integer arithmetic.
+// Digits.  q = round(v 2^k) (|q| <= 2^(8L-2)) has the balanced base-256 digits
+// q = sum_s d_s 256^(L-1-s), d_0 in [-65, 65], d_1.. in [-128, 127].  Adding
+// C = 0x80..80 (L-1 bytes of 128) makes every lower byte of u = q + C equal to
+// d_s + 128 with no carries, and u >> 8(L-1) = d_0; the int8 bit pattern of d_s
+// is then (byte of u) ^ 0x80.  slice_halves returns the two 32-bit halves of u
+// (for L <= 6 straight from one FP64 add: |u| < 2^51 rounds q to nearest even
+// into the low mantissa bits of u + 1.5 * 2^52).
 template <int L>
-__device__ __forceinline__ void to_digits(double v, int e, int (&d)[L]) {
-  const int k = 8 * L - 2 - e;
+__device__ __forceinline__ void slice_halves(double scaled, int& lo, int& hi) {
+  constexpr unsigned long long C = (1ull << (8 * (L - 1))) / 255ull * 128ull;   // 0x8080..80
+  if constexpr (L <= 6) {
+    const double t = scaled + (6755399441055744.0 + double(C));
+    lo = __double2loint(t);
+    hi = __double2hiint(t) - 0x43380000;
+  } else {
+    const long long u = __double2ll_rn(scaled) + (long long)C;
+    lo = int(u);
+    hi = int(u >> 32);
+  }
+}
+
+// v * 2^k rounded into slice_halves; k outside the normal range falls back to scalbn.
+template <int L>
+__device__ __forceinline__ void scale_halves(double v, int k, int& lo, int& hi) {
   const double scaled = (k >= -1022 && k <= 1023) ? v * __longlong_as_double((long long)(k + 1023) << 52)
                                                   : scalbn(v, k);
-  const long long q = __double2ll_rn(scaled);   // |q| <= 2^(8L-2) <= 2^54
-  int x = int(uint32_t(q) & 0xFFFFFFu);
-#pragma unroll
-  for (int s = L - 1; s >= L - 3; --s) {
-    const int dd = ((x + 128) & 255) - 128;
-    d[s] = dd;
-    x = (x - dd) >> 8;
+  slice_halves<L>(scaled, lo, hi);
+}
+
+// Digit planes of 4 consecutive values (a 4 x 4 byte transpose per 32-bit half):
+// w[s] byte i = int8 digit d_s of value i.
+template <int L>
+__device__ __forceinline__ void pack4(const int (&lo)[4], const int (&hi)[4], uint32_t (&w)[L]) {
+  const uint32_t a = __byte_perm(lo[0], lo[1], 0x5140), b = __byte_perm(lo[0], lo[1], 0x7362);
+  const uint32_t c = __byte_perm(lo[2], lo[3], 0x5140), d = __byte_perm(lo[2], lo[3], 0x7362);
+  w[L - 1] = __byte_perm(a, c, 0x5410) ^ 0x80808080u;   // byte 0 of u: the last digit
+  w[L - 2] = __byte_perm(a, c, 0x7632) ^ 0x80808080u;
+  w[L - 3] = __byte_perm(b, d, 0x5410) ^ 0x80808080u;
+  w[L - 4] = __byte_perm(b, d, 0x7632) ^ 0x80808080u;
+  const uint32_t e = __byte_perm(hi[0], hi[1], 0x5140), f = __byte_perm(hi[2], hi[3], 0x5140);
+  if constexpr (L == 6) {
+    w[1] = __byte_perm(e, f, 0x5410) ^ 0x80808080u;
+    w[0] = __byte_perm(e, f, 0x7632);                   // byte 1 of hi: d_0 (no bias)
+  } else {
+    static_assert(L == 7, "6 or 7 digit levels");
+    w[2] = __byte_perm(e, f, 0x5410) ^ 0x80808080u;
+    w[1] = __byte_perm(e, f, 0x7632) ^ 0x80808080u;
+    const uint32_t g = __byte_perm(hi[0], hi[1], 0x0062), h = __byte_perm(hi[2], hi[3], 0x0062);
+    w[0] = __byte_perm(g, h, 0x5410);                   // byte 2 of hi: d_0
   }
-  int y = int(q >> 24) + x;   // x = carry out of the low 24 bits (0 or 1)
-#pragma unroll
-  for (int s = L - 4; s >= 1; --s) {
-    const int dd = ((y + 128) & 255) - 128;
-    d[s] = dd;
-    y = (y - dd) >> 8;
-  }
-  d[0] = y;
 }
 
 // frexp exponent of a nonnegative double given by its bits (0 for zero)
@@ -181,22 +206,18 @@ __global__ void __launch_bounds__(256) slice_planes_kernel(const double* __restr
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
     }
-    uint32_t w[L][4];
+    uint32_t w[4][L];
 #pragma unroll
-    for (int s = 0; s < L; ++s)
+    for (int g4 = 0; g4 < 4; ++g4) {
+      int lo[4], hi[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[s][q] = 0u;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      int d[L];
-      to_digits<L>(v[i], ex[i], d);
-#pragma unroll
-      for (int s = 0; s < L; ++s) w[s][i / 4] |= (uint32_t(d[s]) & 0xFFu) << (8 * (i % 4));
+      for (int i = 0; i < 4; ++i) scale_halves<L>(v[4 * g4 + i], 8 * L - 2 - ex[4 * g4 + i], lo[i], hi[i]);
+      pack4<L>(lo, hi, w[g4]);
     }
     int8_t* blk = planes + ((mb * njb + j / BK) * L) * int64_t(TILE) + (j % BK) * BM + (m0 % BM);
 #pragma unroll
     for (int s = 0; s < L; ++s)
-      *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+      *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[0][s], w[1][s], w[2][s], w[3][s]);
   }
 }
 
@@ -214,23 +235,20 @@ struct BSpec {
 
 constexpr int EXP_NONE = int(0x80808080);   // memset(0x80) sentinel: column chunk has no nonzero
 
-// frexp exponent of |v| * 2^add (EXP_NONE for zero), without the multiply
-__device__ __forceinline__ int exp_of(double v, int add) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7FFFFFFFFFFFFFFFull;
-  if (bits == 0ull) return EXP_NONE;
-  return exp_of_bits(bits) + add;
-}
-
 // B preparation works on whole 128-deep k blocks (one GEMM B stage each): block
 // = 8 warps x 16 rows, lane = column (coalesced factor-row loads), H = column
-// halves (R <= 32: 1, else 2).  NF = number of Khatri-Rao factors when 1..3: the
-// warp's first row is decomposed into factor rows once and later rows advance a
-// mixed-radix cursor (no divisions; all 16 rows' loads in flight); NF = 0: any
-// count, one decomposition per row.
+// halves (R <= 32: 1, else 2).  NF = number of Khatri-Rao factors when 1..3:
+// the warp's first row is decomposed into factor rows once and later rows
+// advance per-factor row pointers (first factor fastest; no divisions, all 16
+// rows' loads independent); NF = 0: any count, one decomposition per row.
+// v[i][h] = KRP[k0 + i, lane + 32 h] (0 outside the tensor / rank);
+// sc[i] = 2^rowexp[k0 + i] (1 without row exponents).
 template <int NF, int H>
 __device__ __forceinline__ void krp_rows16(const BSpec& s, int64_t k0, int lane, double (&v)[16][H],
-                                           int (&add)[16]) {
+                                           double (&sc)[16]) {
+  const bool full = k0 + 16 <= s.K;
   if constexpr (NF > 0) {
+    const double* p[NF];
     uint32_t dig[NF];
     int64_t q = k0 < s.K ? k0 : 0;
 #pragma unroll
@@ -240,25 +258,29 @@ __device__ __forceinline__ void krp_rows16(const BSpec& s, int64_t k0, int lane,
     }
     dig[NF - 1] = uint32_t(q);
 #pragma unroll
+    for (int f = 0; f < NF; ++f) p[f] = s.ptr[f] + size_t(dig[f]) * s.R + lane;
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int64_t k = k0 + i;
-      const bool in = k < s.K;
+      const bool in = full || k0 + i < s.K;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const int r = lane + 32 * h;
-        double p = 1.0;
+        const bool ok = in && lane + 32 * h < s.R;
+        double prod = ok ? __ldg(p[0] + 32 * h) : 0.0;
 #pragma unroll
-        for (int f = 0; f < NF; ++f) p *= (in && r < s.R) ? __ldg(s.ptr[f] + size_t(dig[f]) * s.R + r) : 0.0;
-        v[i][h] = p;
+        for (int f = 1; f < NF; ++f) prod *= ok ? __ldg(p[f] + 32 * h) : 0.0;
+        v[i][h] = prod;
       }
-      add[i] = (s.rowexp && in) ? __ldg(s.rowexp + k) : 0;
       // advance the cursor (first factor fastest)
       ++dig[0];
+      p[0] += s.R;
 #pragma unroll
       for (int f = 0; f < NF - 1; ++f) {
-        const bool wrap = dig[f] == uint32_t(s.dim[f]);
-        dig[f] = wrap ? 0u : dig[f];
-        dig[f + 1] += wrap ? 1u : 0u;
+        if (dig[f] == uint32_t(s.dim[f])) {
+          dig[f] = 0;
+          p[f] -= s.dim[f] * s.R;
+          ++dig[f + 1];
+          p[f + 1] += s.R;
+        }
       }
     }
   } else {
@@ -285,36 +307,52 @@ __device__ __forceinline__ void krp_rows16(const BSpec& s, int64_t k0, int lane,
       }
 #pragma unroll
       for (int h = 0; h < H; ++h) v[i][h] = p[h];
-      add[i] = (s.rowexp && in) ? __ldg(s.rowexp + k) : 0;
+    }
+  }
+  // row scales 2^rowexp (right side); the warp's 16 rows start 16-aligned
+  if (s.rowexp != nullptr && full) {
+    const int4* re = reinterpret_cast<const int4*>(s.rowexp + k0);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int4 e4 = __ldg(re + q4);
+      sc[4 * q4 + 0] = __longlong_as_double((long long)(e4.x + 1023) << 52);
+      sc[4 * q4 + 1] = __longlong_as_double((long long)(e4.y + 1023) << 52);
+      sc[4 * q4 + 2] = __longlong_as_double((long long)(e4.z + 1023) << 52);
+      sc[4 * q4 + 3] = __longlong_as_double((long long)(e4.w + 1023) << 52);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = (s.rowexp != nullptr && k0 + i < s.K) ? __ldg(s.rowexp + k0 + i) : 0;
+      sc[i] = __longlong_as_double((long long)(e + 1023) << 52);
     }
   }
 }
 
-// bexp[chunk][r] = max over the chunk's rows of the frexp exponent of |B[k, r]|
-// (B = KRP times 2^rowexp[k]); one atomic per k block and column.
+// bexp[chunk][r] = frexp exponent of the chunk's max |B[k, r]| (B = KRP times
+// 2^rowexp[k]); one atomic per k block and column.
 template <int NF, int H>
 __global__ void __launch_bounds__(256) bslice_exp_kernel(BSpec s, int* __restrict__ bexp) {
-  __shared__ int red[8][kMaxRank];
+  __shared__ double red[8][kMaxRank];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t kb0 = int64_t(blockIdx.x) * BK;
-  double v[16][H];
-  int add[16];
-  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, add);
+  double v[16][H], sc[16];
+  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, sc);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    int mx = EXP_NONE;
+    double mx = 0.0;
     if (h < H) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) mx = max(mx, exp_of(v[i][h < H ? h : 0], add[i]));
+      for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(v[i][h < H ? h : 0] * sc[i]));
     }
     red[warp][lane + 32 * h] = mx;
   }
   __syncthreads();
   if (threadIdx.x < s.R) {
-    int m = red[0][threadIdx.x];
+    double m = red[0][threadIdx.x];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m = max(m, red[w][threadIdx.x]);
-    if (m != EXP_NONE) atomicMax(bexp + (kb0 / s.Kc) * s.RP + threadIdx.x, m);
+    for (int w = 1; w < 8; ++w) m = fmax(m, red[w][threadIdx.x]);
+    if (m > 0.0) atomicMax(bexp + (kb0 / s.Kc) * s.RP + threadIdx.x, exp_of_bits(__double_as_longlong(m)));
   }
 }
 
@@ -328,33 +366,21 @@ __global__ void __launch_bounds__(256) bslice_digits_kernel(BSpec s, const int* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t kb0 = int64_t(blockIdx.x) * BK;
   const int64_t chunk = kb0 / s.Kc;
-  int e[H];
-#pragma unroll
-  for (int h = 0; h < H; ++h) {
-    const int r = lane + 32 * h;
-    e[h] = r < s.R ? bexp[chunk * s.RP + r] : EXP_NONE;
-  }
-  double v[16][H];
-  int add[16];
-  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, add);
+  double v[16][H], sc[16];
+  krp_rows16<NF, H>(s, kb0 + warp * 16, lane, v, sc);
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     const int r = lane + 32 * h;
     if (r >= s.RP) continue;
+    const int e = r < s.R ? bexp[chunk * s.RP + r] : EXP_NONE;
+    const int k = 8 * L - 2 - (e == EXP_NONE ? 0 : e);   // digits of (v 2^rowexp) / 2^e
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
+      int lo[4], hi[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) scale_halves<L>(v[4 * g + i][h] * sc[4 * g + i], k, lo[i], hi[i]);
       uint32_t w[L];
-#pragma unroll
-      for (int t = 0; t < L; ++t) w[t] = 0u;
-      if (e[h] != EXP_NONE) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          int d[L];
-          to_digits<L>(v[4 * g + i][h], e[h] - add[4 * g + i], d);   // (v 2^add) / 2^e
-#pragma unroll
-          for (int t = 0; t < L; ++t) w[t] |= (uint32_t(d[t]) & 0xFFu) << (8 * i);
-        }
-      }
+      pack4<L>(lo, hi, w);
 #pragma unroll
       for (int t = 0; t < L; ++t) tile[(t * s.RP + r) * 33 + warp * 4 + g] = w[t];
     }
@@ -363,6 +389,191 @@ __global__ void __launch_bounds__(256) bslice_digits_kernel(BSpec s, const int* 
   const int nwords = L * s.RP * (BK / 4);
   uint32_t* dst = reinterpret_cast<uint32_t*>(bs + (kb0 / BK) * int64_t(L) * s.RP * BK);
   for (int q = threadIdx.x; q < nwords; q += blockDim.x) dst[q] = tile[(q >> 5) * 33 + (q & 31)];
+}
+
+// Segment-reuse B preparation for NF >= 2 Khatri-Rao factors whose first
+// (fastest) factor has a multiple of 128 rows: k block kb = seg + nseg * o covers
+// rows 128 seg .. 128 seg + 127 of factor 0 at the o-th combination of the other
+// factors, so a block keeps its 128 factor-0 rows in registers (warp = 16 rows,
+// lane = column) and sweeps G outer indices o, multiplying by one row of the
+// other factors each: every factor row is read once per block instead of once
+// per KRP row.  Each lane's 16 consecutive rows give 16 consecutive bytes of
+// each digit plane (one 16-byte store per plane, no transpose).
+constexpr int SEG_G = 16;   // outer indices per block
+
+template <int NF, int H>
+struct SegCursor {
+  const double* p[NF];      // p[0] fixed: factor-0 rows of the segment; p[1..] advance with o
+  uint32_t dig[NF];
+  __device__ __forceinline__ void init(const BSpec& s, int64_t o0, int lane) {
+    int64_t q = o0;
+#pragma unroll
+    for (int f = 1; f < NF - 1; ++f) {
+      dig[f] = uint32_t(q % s.dim[f]);
+      q /= s.dim[f];
+    }
+    dig[NF - 1] = uint32_t(q);
+#pragma unroll
+    for (int f = 1; f < NF; ++f) p[f] = s.ptr[f] + size_t(dig[f]) * s.R + lane;
+  }
+  __device__ __forceinline__ void advance(const BSpec& s) {
+    ++dig[1];
+    p[1] += s.R;
+#pragma unroll
+    for (int f = 1; f < NF - 1; ++f) {
+      if (dig[f] == uint32_t(s.dim[f])) {
+        dig[f] = 0;
+        p[f] -= s.dim[f] * s.R;
+        ++dig[f + 1];
+        p[f + 1] += s.R;
+      }
+    }
+  }
+};
+
+// Per outer index o: the 16 row exponents of the warp's rows (4 x int4) and the
+// product g of the other factors' entries, loaded one o ahead (prefetch).
+template <int NF, int H>
+struct SegLoads {
+  int4 re[4];
+  double g[H];
+  __device__ __forceinline__ void load(const BSpec& s, const SegCursor<NF, H>& cur, int64_t k0, int lane,
+                                       bool valid) {
+    if (s.rowexp != nullptr && valid) {
+      const int4* p = reinterpret_cast<const int4*>(s.rowexp + k0);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) re[q4] = __ldg(p + q4);
+    } else {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) re[q4] = make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      double gg = 1.0;
+#pragma unroll
+      for (int f = 1; f < NF; ++f) gg *= (valid && lane + 32 * h < s.R) ? __ldg(cur.p[f] + 32 * h) : 0.0;
+      g[h] = gg;
+    }
+  }
+  __device__ __forceinline__ int rexp(int i) const {
+    const int4 v = re[i >> 2];
+    return (i & 3) == 0 ? v.x : (i & 3) == 1 ? v.y : (i & 3) == 2 ? v.z : v.w;
+  }
+};
+
+template <int NF, int H>
+__global__ void __launch_bounds__(256) bseg_exp_kernel(BSpec s, int* __restrict__ bexp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nseg = s.dim[0] / BK, outer = s.K / s.dim[0];
+  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * SEG_G;
+  const int64_t i0 = seg * BK + warp * 16;        // first factor-0 row of the warp
+  double h0[16][H];
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      h0[i][h] = lane + 32 * h < s.R ? __ldg(s.ptr[0] + (i0 + i) * s.R + lane + 32 * h) : 0.0;
+  SegCursor<NF, H> cur;
+  cur.init(s, o0, lane);
+  double mx[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) mx[h] = 0.0;
+  int64_t chunk = -1;
+  const int64_t oend = min(outer, o0 + SEG_G);
+  SegLoads<NF, H> nxt;
+  nxt.load(s, cur, i0 + s.dim[0] * o0, lane, o0 < oend);
+  for (int64_t o = o0; o < oend; ++o) {
+    const SegLoads<NF, H> now = nxt;
+    cur.advance(s);
+    nxt.load(s, cur, i0 + s.dim[0] * (o + 1), lane, o + 1 < oend);
+    const int64_t c = (seg + nseg * o) * BK / s.Kc;
+    if (c != chunk) {
+      if (chunk >= 0) {
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          if (lane + 32 * h < s.R && mx[h] > 0.0)
+            atomicMax(bexp + chunk * s.RP + lane + 32 * h, exp_of_bits(__double_as_longlong(mx[h])));
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h) mx[h] = 0.0;
+      chunk = c;
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double sc = __longlong_as_double((long long)(now.rexp(i) + 1023) << 52);
+        mx[h] = fmax(mx[h], fabs(h0[i][h] * now.g[h] * sc));
+      }
+    }
+  }
+  if (chunk >= 0) {
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      if (lane + 32 * h < s.R && mx[h] > 0.0)
+        atomicMax(bexp + chunk * s.RP + lane + 32 * h, exp_of_bits(__double_as_longlong(mx[h])));
+  }
+}
+
+template <int L, int NF, int H>
+__global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __restrict__ bexp,
+                                                          int8_t* __restrict__ bs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nseg = s.dim[0] / BK, outer = s.K / s.dim[0];
+  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * SEG_G;
+  const int64_t i0 = seg * BK + warp * 16;
+  double h0[16][H];
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      h0[i][h] = lane + 32 * h < s.R ? __ldg(s.ptr[0] + (i0 + i) * s.R + lane + 32 * h) : 0.0;
+  SegCursor<NF, H> cur;
+  cur.init(s, o0, lane);
+  const int64_t oend = min(outer, o0 + SEG_G);
+  for (int64_t o = o0; o < oend; ++o) {
+    const int64_t k0 = i0 + s.dim[0] * o;
+    const int64_t kb = seg + nseg * o;
+    const int64_t c = kb * BK / s.Kc;
+    double sc[16];
+    if (s.rowexp != nullptr) {
+      const int4* re = reinterpret_cast<const int4*>(s.rowexp + k0);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int4 e4 = __ldg(re + q4);
+        sc[4 * q4 + 0] = __longlong_as_double((long long)(e4.x + 1023) << 52);
+        sc[4 * q4 + 1] = __longlong_as_double((long long)(e4.y + 1023) << 52);
+        sc[4 * q4 + 2] = __longlong_as_double((long long)(e4.z + 1023) << 52);
+        sc[4 * q4 + 3] = __longlong_as_double((long long)(e4.w + 1023) << 52);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sc[i] = 1.0;
+    }
+    int8_t* blk = bs + kb * int64_t(L) * s.RP * BK + warp * 16;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int r = lane + 32 * h;
+      if (r >= s.RP) continue;
+      const int e = r < s.R ? __ldg(bexp + c * s.RP + r) : EXP_NONE;
+      const int kx = 8 * L - 2 - (e == EXP_NONE ? 0 : e);
+      double g = 1.0;
+#pragma unroll
+      for (int f = 1; f < NF; ++f) g *= r < s.R ? __ldg(cur.p[f] + 32 * h) : 0.0;
+      uint32_t w[4][L];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        int lo[4], hi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) scale_halves<L>(h0[4 * q4 + i][h] * g * sc[4 * q4 + i], kx, lo[i], hi[i]);
+        pack4<L>(lo, hi, w[q4]);
+      }
+#pragma unroll
+      for (int t = 0; t < L; ++t)
+        *reinterpret_cast<uint4*>(blk + (int64_t(t) * s.RP + r) * BK) = make_uint4(w[0][t], w[1][t], w[2][t], w[3][t]);
+    }
+    cur.advance(s);
+  }
 }
 
 template <int L, int NF, int H>
@@ -380,9 +591,24 @@ int launch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaS
   return NNCP_OK;
 }
 
+template <int L, int NF, int H>
+int launch_bseg(const BSpec& b, int* bexp, int8_t* bs, cudaStream_t st) {
+  const int64_t outer = b.K / b.dim[0];
+  const dim3 grid{unsigned(b.dim[0] / BK), unsigned((outer + SEG_G - 1) / SEG_G), 1u};
+  bseg_exp_kernel<NF, H><<<grid, 256, 0, st>>>(b, bexp);
+  NNCP_LAUNCH_CHECK();
+  bseg_digits_kernel<L, NF, H><<<grid, 256, 0, st>>>(b, bexp, bs);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
 template <int L, int NF>
 int launch_bslice_h(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaStream_t st) {
-  // the cursor path needs dims below 2^32 (always: factor rows are int32-indexed)
+  // segment reuse when factor 0 tiles into whole k blocks (then K = dim[0] * outer is too)
+  if (NF >= 2 && b.dim[0] % BK == 0 && b.K / b.dim[0] < 65535 * SEG_G) {
+    constexpr int NS = NF >= 2 ? NF : 2;
+    return b.RP <= 32 ? launch_bseg<L, NS, 1>(b, bexp, bs, st) : launch_bseg<L, NS, 2>(b, bexp, bs, st);
+  }
   return b.RP <= 32 ? launch_bslice<L, NF, 1>(b, bexp, bs, kblocks, st)
                     : launch_bslice<L, NF, 2>(b, bexp, bs, kblocks, st);
 }
@@ -521,7 +747,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
     }
     for (int i = 0; i < C::NBUF; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 8);
     }
     fence_barrier_init();
   }
@@ -627,7 +853,9 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
     }
   } else {
     // -------------------------------------------------- epilogue --------
-    const int quad = warp & 3;
+    // warp w: TMEM lane quadrant w % 4 (rows), column half (w - 2) / 4
+    constexpr int RH = RP / 2;
+    const int quad = warp & 3, half = (warp - 2) >> 2;
     int abuf = 0;
     uint32_t tph = 0;
     for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
@@ -636,21 +864,21 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
       const int64_t row = tile * BM + quad * 32 + lane;
       const bool valid = row < a.rows;
       const int ex = (a.rowexp != nullptr && valid) ? a.rowexp[row] : 0;
-      double acc[RP];
+      double acc[RH];
 #pragma unroll
-      for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+      for (int r = 0; r < RH; ++r) acc[r] = 0.0;
       for (int64_t c = c0; c < c1; ++c) {
         mbar_wait(&tfull[abuf], tph);
         tc_fence_after();
-        const uint32_t taddr = tbase + uint32_t(abuf * C::ACC) + (uint32_t(quad * 32) << 16);
-        int eb[RP];   // column-chunk exponents, with the 2^-12 of the two digit scales
+        const uint32_t taddr = tbase + uint32_t(abuf * C::ACC + half * RH) + (uint32_t(quad * 32) << 16);
+        int eb[RH];   // column-chunk exponents, with the 2^-12 of the two digit scales and the row scale
 #pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          const int e = __ldg(a.bexp + c * RP + r);
-          eb[r] = (e == EXP_NONE ? 0 : e) - 12;   // an all-zero column chunk accumulated zeros
+        for (int r = 0; r < RH; ++r) {
+          const int e = __ldg(a.bexp + c * RP + half * RH + r);
+          eb[r] = (e == EXP_NONE ? 0 : e) - 12 + ex;   // an all-zero column chunk accumulated zeros
         }
 #pragma unroll
-        for (int rg = 0; rg < RP / 8; ++rg) {
+        for (int rg = 0; rg < RH / 8; ++rg) {
           uint32_t v[L][8];
 #pragma unroll
           for (int l = 0; l < L; ++l) tmem_ld8(taddr + uint32_t(l * RP + rg * 8), v[l]);
@@ -660,7 +888,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
             double s = double(int(v[L - 1][i]));
 #pragma unroll
             for (int l = L - 2; l >= 0; --l) s = fma(s, 0.00390625, double(int(v[l][i])));
-            acc[rg * 8 + i] += times_pow2(s, ex + eb[rg * 8 + i]);
+            acc[rg * 8 + i] += times_pow2(s, eb[rg * 8 + i]);
           }
         }
         tc_fence_before();
@@ -674,8 +902,8 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
       if (valid) {
         double* o = a.out + g * a.group_stride + row;
 #pragma unroll
-        for (int r = 0; r < RP; ++r)
-          if (r < a.R) o[int64_t(r) * a.rows] = acc[r];
+        for (int r = 0; r < RH; ++r)
+          if (half * RH + r < a.R) o[int64_t(half * RH + r) * a.rows] = acc[r];
       }
     }
   }
@@ -724,8 +952,11 @@ CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank
   } else {
     // split the contraction into groups so row_tiles x groups fills the SMs; the
     // row tiles of a group stream the same B chunks at the same time (L2 reuse)
+    // Chunk length chosen so every group gets the same number of chunks (q).
     const int64_t want = std::max<int64_t>(1, sms / p.row_tiles);
-    p.Kc = std::min<int64_t>(KC_MAX, std::max<int64_t>(256, align_up((p.Kp + want - 1) / want, 256)));
+    const int64_t per_group = (p.Kp + want - 1) / want;
+    const int64_t q = std::max<int64_t>(1, (per_group + KC_MAX - 1) / KC_MAX);
+    p.Kc = std::min<int64_t>(KC_MAX, std::max<int64_t>(256, align_up((p.Kp + want * q - 1) / (want * q), 256)));
     const int64_t nch = (p.Kp + p.Kc - 1) / p.Kc;
     p.groups = int(std::min<int64_t>(want, nch));
   }
