@@ -47,3 +47,26 @@ def test_device_calls_fail_loudly_without_gpu():
 
     with pytest.raises(RuntimeError, match="CUDA device"):
         P.gram([[1.0, 2.0], [3.0, 4.0]])
+
+
+def test_sliced_sizing_entry_points():
+    """Host-side sizing / validation of the sliced (int8 tensor-core) MTTKRP path."""
+    from paper_1909_01149_b200 import _lib
+    from paper_1909_01149_b200.dimtree import DimTreePlan, SlicedTensor
+
+    lib = _lib.load(require_device=False)
+    # 2048^3, split 2: int32 row exponents + uint64 row maxima + 6 planes of 128x128-blocked digits
+    m, j = 2048 * 2048, 2048
+    expect = 1024 + (m * 4 + m * 8) + 6 * m * j
+    assert SlicedTensor.nbytes((2048, 2048, 2048), 2) == expect
+    assert SlicedTensor.nbytes((2048, 2048, 2048), 2, levels=7) == expect + m * j
+    # padding of ragged unfoldings to whole 128 x 128 blocks
+    assert SlicedTensor.nbytes((7, 9, 11), 2) >= 6 * 128 * 128
+    p = DimTreePlan.create((2048, 2048, 2048), 32)
+    ws = p.sliced_workspace_bytes()
+    # right side: factor digits 6 x 32 x M bytes dominate
+    assert 6 * 32 * m <= ws < 6 * 32 * m + (64 << 20)
+    assert lib.nncp_sliced_workspace_bytes(3, _lib.i64([64, 64, 64]), 0, 8, 6) == 0     # bad split
+    out = ctypes.c_size_t(0)
+    assert lib.nncp_sliced_tensor_bytes(3, _lib.i64([64, 64, 64]), 2, 5, ctypes.byref(out)) == _lib.NNCP_ERR_UNSUPPORTED
+    assert lib.nncp_sliced_tensor_bytes(3, _lib.i64([64, 64, 64]), 3, 6, ctypes.byref(out)) == _lib.NNCP_ERR_VALUE
