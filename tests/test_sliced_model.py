@@ -1,0 +1,80 @@
+"""The sliced-tensor MTTKRP algorithm (tests/sliced_model.py, a bit-exact model of
+the int8 tensor-core kernels) against the oracle on the CPU, and the CUDA
+kernels against the model bit for bit on the GPU."""
+
+import numpy as np
+import pytest
+
+from oracle import nncp_oracle as O
+from tests.conftest import rel_fro
+from tests.sliced_model import plan, sliced_partial
+
+MTTKRP_TOL = 1e-12
+
+CASES = [((7, 9, 11), 5), ((33, 17, 5), 1), ((96, 64, 48), 20), ((256, 130, 40), 8), ((128, 24, 30, 8), 12),
+         ((20, 18, 16, 14), 33), ((256, 256, 64), 8), ((40, 40, 20000), 4)]
+
+
+def _case(dims, r, signed=False):
+    rng = np.random.default_rng(sum(dims) * 7 + r)
+    x = rng.random(int(np.prod(dims)))
+    hs = [rng.random((d, r)) for d in dims]
+    if signed:
+        x = x - 0.4
+        hs = [h - 0.3 for h in hs]
+    return x, hs
+
+
+@pytest.mark.parametrize("dims,r", CASES)
+def test_model_matches_oracle(dims, r):
+    x, hs = _case(dims, r)
+    from paper_1909_01149_b200.dimtree import choose_split_mode
+
+    s = choose_split_mode(dims)
+    for side, fn in (("left", O.partial_left), ("right", O.partial_right)):
+        got = sliced_partial(x, dims, s, side, hs, r)
+        assert rel_fro(got, fn(x, dims, s, hs)) <= MTTKRP_TOL, (side, dims, r)
+
+
+def test_model_levels7_and_signs():
+    dims, r = (96, 64, 48), 20
+    x, hs = _case(dims, r, signed=True)
+    for levels, tol in ((6, 1e-12), (7, 1e-14)):
+        for side, fn in (("left", O.partial_left), ("right", O.partial_right)):
+            got = sliced_partial(x, dims, 2, side, hs, r, levels=levels)
+            want = fn(x, dims, 2, hs)
+            absref = fn(np.abs(x), dims, 2, [np.abs(h) for h in hs])
+            assert np.max(np.abs(got - want) / absref) <= tol, (levels, side)
+
+
+def test_plan_splits_contraction_evenly():
+    p = plan((2048, 2048, 2048), 2, "right", 32)
+    assert p["groups"] == 9 and p["nchunks"] % p["groups"] == 0 and p["Kc"] <= 16384
+    p = plan((1024, 1024, 1024), 2, "right", 32)
+    assert p["groups"] == 18 and p["nchunks"] % p["groups"] == 0
+    p = plan((2048, 2048, 2048), 2, "left", 32)
+    assert p["groups"] == 1 and p["nchunks"] == 1
+    p = plan((40, 40, 20000), 2, "left", 4)
+    assert p["nchunks"] == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,r", CASES)
+def test_kernels_bitwise_equal_model(dims, r):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1909_01149_b200 as P
+    from paper_1909_01149_b200 import _lib
+    from paper_1909_01149_b200.dimtree import SlicedTensor
+
+    sms = _lib.load().nncp_device_sms()
+    x, hs = _case(dims, r, signed=(r % 2 == 1))
+    plan_ = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    sl = SlicedTensor(xd, dims, plan_.split)
+    for side in ("left", "right"):
+        got = P.partial_mttkrp(xd, hs, side, plan_, sliced=sl).data.cpu().numpy()
+        want = sliced_partial(x, dims, plan_.split, side, hs, r, sms=sms)
+        assert np.array_equal(got, want), (side, dims, r, float(np.max(np.abs(got - want))))
