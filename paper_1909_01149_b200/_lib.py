@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnncp_b200.so")
+# NNCP_LIB_PATH: an instrumented build for the tools (tools/sliced_stats.py); never set by the product
+LIB_PATH = os.environ.get("NNCP_LIB_PATH") or os.path.join(_HERE, "libnncp_b200.so")
 
 NNCP_OK = 0
 NNCP_ERR_VALUE = 1

@@ -28,9 +28,9 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, extra=(), tag: str = "") -> tuple[str, str]:
+    obj = os.path.join(BUILD, src.replace(".cu", tag + ".o"))
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
@@ -54,5 +54,17 @@ def build(verbose: bool = False) -> str:
     return OUT
 
 
+def build_stats() -> str:
+    """Instrumented variant (barrier wait counters in the sliced GEMM) for tools/sliced_stats.py."""
+    out = os.path.join(HERE, "libnncp_b200_stats.so")
+    os.makedirs(BUILD, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = [o for o, _ in ex.map(lambda s: _compile(s, ("-DNNCP_SLICED_STATS",), "_stats"), SOURCES)]
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-lcudart"], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    return out
+
+
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build_stats() if "--stats" in sys.argv else build(verbose="-v" in sys.argv))

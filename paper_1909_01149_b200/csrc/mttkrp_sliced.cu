@@ -689,6 +689,20 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 }
 
 // --------------------------------------------------------------- GEMM ---
+// Build with -DNNCP_SLICED_STATS for per-CTA barrier wait cycles (tools only):
+// [0] producer on B empty, [1] producer on A empty, [2] MMA on TMEM empty,
+// [3] MMA on B full, [4] MMA on A full, [5] epilogue on TMEM full, [6] kernel cycles.
+#ifdef NNCP_SLICED_STATS
+__device__ unsigned long long g_sliced_stats[1024 * 8];
+#define SLICED_WAIT(slot, bar, par)                                              \
+  do {                                                                           \
+    const long long _t0 = clock64();                                             \
+    mbar_wait(bar, par);                                                         \
+    atomicAdd(&g_sliced_stats[blockIdx.x * 8 + (slot)], (unsigned long long)(clock64() - _t0)); \
+  } while (0)
+#else
+#define SLICED_WAIT(slot, bar, par) mbar_wait(bar, par)
+#endif
 template <int RP, int L>
 struct GemmCfg {
   static constexpr int A_STAGE = TILE;                  // one digit-plane tile
@@ -764,6 +778,9 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
+#ifdef NNCP_SLICED_STATS
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -774,7 +791,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
         const int64_t tile = it % a.row_tiles, g = it / a.row_tiles;
         const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
         for (int64_t kb = c0 * a.kbc, kend = min(a.nkb, c1 * a.kbc); kb < kend; ++kb) {
-          mbar_wait(&bempty[bsx], bph ^ 1u);
+          SLICED_WAIT(0, &bempty[bsx], bph ^ 1u);
           mbar_arrive_expect_tx(&bfull[bsx], C::B_STAGE);
           tma_load_4d(smem_b + size_t(bsx) * C::B_STAGE, &mapB, &bfull[bsx], 0, 0, 0, int(kb));
           if (++bsx == C::NB) {
@@ -784,7 +801,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
           const int mb = int(LEFT ? tile : kb), jb = int(LEFT ? kb : tile);
 #pragma unroll 1
           for (int s = 0; s < L; ++s) {
-            mbar_wait(&aempty[as], aph ^ 1u);
+            SLICED_WAIT(1, &aempty[as], aph ^ 1u);
             mbar_arrive_expect_tx(&afull[as], C::A_STAGE);
             tma_load_5d(smem_a + size_t(as) * C::A_STAGE, &mapA, &afull[as], 0, 0, s, jb, mb);
             if (++as == C::NA) {
@@ -804,28 +821,28 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
         const int64_t g = it / a.row_tiles;
         const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
         for (int64_t c = c0; c < c1; ++c) {
-          mbar_wait(&tempty[abuf], tph ^ 1u);
+          SLICED_WAIT(2, &tempty[abuf], tph ^ 1u);
           tc_fence_after();
           const uint32_t dcol = tbase + uint32_t(abuf * C::ACC);
           bool first = true;
           for (int64_t kb = c * a.kbc, kend = min(a.nkb, (c + 1) * a.kbc); kb < kend; ++kb) {
-            mbar_wait(&bfull[bsx], bph);
+            SLICED_WAIT(3, &bfull[bsx], bph);
             tc_fence_after();
-            const uint32_t sb = smem_u32(smem_b + size_t(bsx) * C::B_STAGE);
-#pragma unroll 1
+            // descriptors of this k block's B stage; every MMA below adds compile-time offsets
+            const uint64_t db0 = smem_desc(smem_u32(smem_b + size_t(bsx) * C::B_STAGE), 1024, 2);
+#pragma unroll
             for (int s = 0; s < L; ++s) {
-              mbar_wait(&afull[as], aph);
+              SLICED_WAIT(4, &afull[as], aph);
               tc_fence_after();
-              const uint32_t sa = smem_u32(smem_a + size_t(as) * C::A_STAGE);
-              const int ntot = (L - s) * RP;
+              const uint64_t da0 = smem_desc(smem_u32(smem_a + size_t(as) * C::A_STAGE), 1024, 2);
 #pragma unroll
               for (int kk = 0; kk < BK / 32; ++kk) {
                 // left: MN-major SW128 (32 k rows of 128 B per MMA); right: K-major SW128 (32 B per MMA)
-                const uint64_t da = LEFT ? smem_desc(sa + kk * 32 * 128, 1024, 2) : smem_desc(sa + kk * 32, 1024, 2);
-#pragma unroll 1
-                for (int n0 = 0; n0 < ntot; n0 += 256) {
-                  const int nn = ntot - n0 < 256 ? ntot - n0 : 256;
-                  const uint64_t db = smem_desc(sb + kk * 32 + (n0 / 8) * 1024, 1024, 2);
+                const uint64_t da = da0 + uint64_t(LEFT ? (kk * 32 * 128) >> 4 : (kk * 32) >> 4);
+#pragma unroll
+                for (int n0 = 0; n0 < (L - s) * RP; n0 += 256) {
+                  const int nn = (L - s) * RP - n0 < 256 ? (L - s) * RP - n0 : 256;
+                  const uint64_t db = db0 + uint64_t((kk * 32 + (n0 / 8) * 1024) >> 4);
                   umma_s8(dcol + uint32_t(s * RP + n0), da, db, idesc_s8(nn, LEFT),
                           (first && s == 0 && kk == 0) ? 0u : 1u);
                 }
@@ -868,7 +885,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
 #pragma unroll
       for (int r = 0; r < RH; ++r) acc[r] = 0.0;
       for (int64_t c = c0; c < c1; ++c) {
-        mbar_wait(&tfull[abuf], tph);
+        SLICED_WAIT(5, &tfull[abuf], tph);
         tc_fence_after();
         const uint32_t taddr = tbase + uint32_t(abuf * C::ACC + half * RH) + (uint32_t(quad * 32) << 16);
         int eb[RH];   // column-chunk exponents, with the 2^-12 of the two digit scales and the row scale
@@ -909,6 +926,9 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
+#ifdef NNCP_SLICED_STATS
+  if (threadIdx.x == 0) g_sliced_stats[blockIdx.x * 8 + 6] += (unsigned long long)(clock64() - t_start);
+#endif
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS));
@@ -1143,3 +1163,15 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
 }
 
 }  // namespace nncp
+
+#ifdef NNCP_SLICED_STATS
+extern "C" int nncp_sliced_stats(unsigned long long* host, int n, int reset) {
+  if (n > 1024 * 8) n = 1024 * 8;
+  if (cudaMemcpyFromSymbol(host, nncp::sliced::g_sliced_stats, sizeof(unsigned long long) * n) != cudaSuccess) return 3;
+  if (reset) {
+    static unsigned long long zeros[1024 * 8];
+    if (cudaMemcpyToSymbol(nncp::sliced::g_sliced_stats, zeros, sizeof(zeros)) != cudaSuccess) return 3;
+  }
+  return 0;
+}
+#endif
