@@ -68,7 +68,8 @@ class RunConfig:
     initial_factors: FactorSet = None
     cuda_graph: bool = None   # None = auto: replay the sweep as a CUDA graph when it is capturable
     # partial-MTTKRP engine: "sliced" = int8 tensor cores over a once-sliced tensor
-    # (DESIGN.md §4.4), "fp64" = FP64 DMMA, "auto" = sliced when the slices fit in HBM
+    # (DESIGN.md §4.4), "fp64" = FP64 DMMA, "auto" = sliced when its cost model wins
+    # and the slices fit in HBM
     mttkrp_kernel: str = "auto"
 
     def validate(self, order: int):
@@ -232,15 +233,24 @@ class _EventTimer:
 
 SLICED_MIN_ELEMS = 1 << 22       # below this the fp64 path's fewer launches win
 SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
+# partial-MTTKRP cost model for mttkrp_kernel="auto" (B200 measurements):
+# FP64 DMMA path reaches ~87% of max(8 I / BW, 2 I R / 37.1 TF); the sliced path streams
+# 6 I bytes at ~6.9 TB/s plus ~90 us of per-call digit prep and launches
+_HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 9e-5
 
 
-def _use_sliced(kind: str, dims, split: int, dev) -> bool:
+def _use_sliced(kind: str, dims, split: int, rank: int, dev) -> bool:
     """Resolve RunConfig.mttkrp_kernel for one execution context."""
     if kind == "fp64":
         return False
     if kind == "sliced":
         return True
-    if int(np.prod(dims)) < SLICED_MIN_ELEMS:
+    size = int(np.prod(dims))
+    if size < SLICED_MIN_ELEMS:
+        return False
+    t_fp64 = max(8.0 * size / _HBM_BPS, 2.0 * size * rank / _DMMA_FLOPS) / 0.87
+    t_sliced = 6.0 * size / _SLICED_BPS + _SLICED_FIXED_S
+    if t_sliced >= t_fp64:
         return False
     free, _ = torch.cuda.mem_get_info(dev)
     return SlicedTensor.nbytes(dims, split) + SLICED_HBM_MARGIN <= free
@@ -273,7 +283,7 @@ class _Engine:
         self.n_owned = [s.stop - s.start for s in self.owned_rows]
         self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
         self.sliced = None
-        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, dev):
+        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, self.R, dev):
             self.sliced = SlicedTensor(x_local, self.dims, self.plan.split)
         ws_bytes = self.plan.workspace_bytes()
         if self.sliced is not None:
