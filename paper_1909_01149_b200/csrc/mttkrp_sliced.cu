@@ -515,13 +515,20 @@ __global__ void __launch_bounds__(256) bseg_exp_kernel(BSpec s, int* __restrict_
   }
 }
 
+// Digits: each warp packs its 16 rows of every (digit, column) row into 16 bytes,
+// staged in shared memory (row pitch 144 B: the 8 lanes of a 16-byte store phase
+// hit distinct banks) so the k block leaves as one contiguous run of full lines.
+constexpr int SEG_PITCH = 144;
+
 template <int L, int NF, int H>
 __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __restrict__ bexp,
                                                           int8_t* __restrict__ bs) {
+  extern __shared__ __align__(16) uint8_t stage[];   // L * RP rows x SEG_PITCH bytes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nseg = s.dim[0] / BK, outer = s.K / s.dim[0];
   const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * SEG_G;
   const int64_t i0 = seg * BK + warp * 16;
+  const int nrow = L * s.RP;
   double h0[16][H];
 #pragma unroll
   for (int i = 0; i < 16; ++i)
@@ -531,48 +538,41 @@ __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __
   SegCursor<NF, H> cur;
   cur.init(s, o0, lane);
   const int64_t oend = min(outer, o0 + SEG_G);
+  SegLoads<NF, H> nxt;
+  nxt.load(s, cur, i0 + s.dim[0] * o0, lane, o0 < oend);
   for (int64_t o = o0; o < oend; ++o) {
-    const int64_t k0 = i0 + s.dim[0] * o;
+    const SegLoads<NF, H> now = nxt;
+    cur.advance(s);
+    nxt.load(s, cur, i0 + s.dim[0] * (o + 1), lane, o + 1 < oend);
     const int64_t kb = seg + nseg * o;
     const int64_t c = kb * BK / s.Kc;
-    double sc[16];
-    if (s.rowexp != nullptr) {
-      const int4* re = reinterpret_cast<const int4*>(s.rowexp + k0);
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int4 e4 = __ldg(re + q4);
-        sc[4 * q4 + 0] = __longlong_as_double((long long)(e4.x + 1023) << 52);
-        sc[4 * q4 + 1] = __longlong_as_double((long long)(e4.y + 1023) << 52);
-        sc[4 * q4 + 2] = __longlong_as_double((long long)(e4.z + 1023) << 52);
-        sc[4 * q4 + 3] = __longlong_as_double((long long)(e4.w + 1023) << 52);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) sc[i] = 1.0;
-    }
-    int8_t* blk = bs + kb * int64_t(L) * s.RP * BK + warp * 16;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int r = lane + 32 * h;
       if (r >= s.RP) continue;
       const int e = r < s.R ? __ldg(bexp + c * s.RP + r) : EXP_NONE;
       const int kx = 8 * L - 2 - (e == EXP_NONE ? 0 : e);
-      double g = 1.0;
-#pragma unroll
-      for (int f = 1; f < NF; ++f) g *= r < s.R ? __ldg(cur.p[f] + 32 * h) : 0.0;
       uint32_t w[4][L];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         int lo[4], hi[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) scale_halves<L>(h0[4 * q4 + i][h] * g * sc[4 * q4 + i], kx, lo[i], hi[i]);
+        for (int i = 0; i < 4; ++i) {
+          const double sc = __longlong_as_double((long long)(now.rexp(4 * q4 + i) + 1023) << 52);
+          scale_halves<L>(h0[4 * q4 + i][h] * now.g[h] * sc, kx, lo[i], hi[i]);
+        }
         pack4<L>(lo, hi, w[q4]);
       }
 #pragma unroll
       for (int t = 0; t < L; ++t)
-        *reinterpret_cast<uint4*>(blk + (int64_t(t) * s.RP + r) * BK) = make_uint4(w[0][t], w[1][t], w[2][t], w[3][t]);
+        *reinterpret_cast<uint4*>(stage + (t * s.RP + r) * SEG_PITCH + warp * 16) =
+            make_uint4(w[0][t], w[1][t], w[2][t], w[3][t]);
     }
-    cur.advance(s);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(bs + kb * int64_t(L) * s.RP * BK);
+    for (int q = threadIdx.x; q < nrow * 8; q += blockDim.x)
+      dst[q] = *reinterpret_cast<const uint4*>(stage + (q >> 3) * SEG_PITCH + (q & 7) * 16);
+    __syncthreads();
   }
 }
 
@@ -597,7 +597,13 @@ int launch_bseg(const BSpec& b, int* bexp, int8_t* bs, cudaStream_t st) {
   const dim3 grid{unsigned(b.dim[0] / BK), unsigned((outer + SEG_G - 1) / SEG_G), 1u};
   bseg_exp_kernel<NF, H><<<grid, 256, 0, st>>>(b, bexp);
   NNCP_LAUNCH_CHECK();
-  bseg_digits_kernel<L, NF, H><<<grid, 256, 0, st>>>(b, bexp, bs);
+  static bool attr = false;
+  if (!attr) {
+    NNCP_CUDA_TRY(cudaFuncSetAttribute(bseg_digits_kernel<L, NF, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(L * kMaxRank * SEG_PITCH)));
+    attr = true;
+  }
+  bseg_digits_kernel<L, NF, H><<<grid, 256, size_t(L) * b.RP * SEG_PITCH, st>>>(b, bexp, bs);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
