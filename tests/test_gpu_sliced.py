@@ -189,3 +189,23 @@ def test_sliced_graph_matches_eager(P):
     assert runs[0].errors == runs[1].errors
     for a, b in zip(runs[0].model.factors, runs[1].model.factors):
         assert np.array_equal(a, b)
+
+
+def test_sliced_grid_runs_vs_golden(P, golden):
+    """Thread-simulated grid runs (one engine, one sliced tensor block per worker) vs the reference's grid runs."""
+    g = golden("runs.npz")
+    for tag in [str(t) for t in g["grids"]]:
+        name = tag[len("grid_"):tag.rindex("_")]
+        grid = tuple(int(v) for v in tag[tag.rindex("_") + 1:].split("x"))
+        dims = tuple(int(d) for d in g[f"{name}_dims"])
+        r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
+        algo = str(g[f"{name}_algo"])
+        x = P.DenseTensor(dims, g[f"{name}_x"])
+        cfg = P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed, grid=grid,
+                          mttkrp_kernel="sliced")
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            par = P.nncp_parallel(x, cfg)
+        assert np.max(np.abs(np.array(par.errors) - g[f"{tag}_errors"])) <= TRACE_TOL, tag
+        for n in range(len(dims)):
+            assert np.max(np.abs(par.model.factors[n] - g[f"{tag}_f{n}"])) <= FACTOR_TOL, (tag, n)

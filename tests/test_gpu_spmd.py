@@ -36,7 +36,8 @@ def _worker(rank, world, port, case, out_q):
         from tests.conftest import load_golden
 
         g = load_golden("runs.npz")
-        name, grid = case
+        name, grid = case[:2]
+        engine = case[2] if len(case) > 2 else "auto"
         dims = tuple(int(d) for d in g[f"{name}_dims"])
         r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
         algo = str(g[f"{name}_algo"])
@@ -44,7 +45,7 @@ def _worker(rank, world, port, case, out_q):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             rep = P.nncp_parallel(x, P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed,
-                                                 grid=grid))
+                                                 grid=grid, mttkrp_kernel=engine))
         out_q.put((rank, rep.errors, [np.asarray(f) for f in rep.model.factors],
                    [rep.counters.calls.get(c, 0) for c in ("ReduceScatter", "AllGather", "AllReduce")]))
     except Exception as exc:  # noqa: BLE001
@@ -53,14 +54,15 @@ def _worker(rank, world, port, case, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [("hals_odd", (2, 2, 1)), ("mu4", (2, 1, 2, 1)), ("bpp3", (2, 2, 2))])
+@pytest.mark.parametrize("case", [("hals_odd", (2, 2, 1)), ("mu4", (2, 1, 2, 1)), ("bpp3", (2, 2, 2)),
+                                  ("bpp3", (2, 2, 2), "sliced"), ("mu4", (2, 1, 2, 1), "sliced")])
 def test_spmd_processes_match_reference_grid_run(golden, case):
     import torch
     import torch.multiprocessing as mp
 
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    name, grid = case
+    name, grid = case[:2]
     world = int(np.prod(grid))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
