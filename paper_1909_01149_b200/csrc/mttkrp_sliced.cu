@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
         double* o = a.out + g * a.group_stride + row;
 #pragma unroll
         for (int r = 0; r < RH; ++r)
-          if (half * RH + r < a.R) o[int64_t(half * RH + r) * a.rows] = acc[r];
+          if (half * RH + r < a.R) __stcs(o + int64_t(half * RH + r) * a.rows, acc[r]);   // streaming store
       }
     }
   }
