@@ -107,10 +107,12 @@ __global__ void __launch_bounds__(kBppWarps * 32)
   double* red = S + RP * RP;                          // kBppWarps * 64
   double* colbuf = red + kBppWarps * 64;              // RP + 1
   double* lu = colbuf + RP + 1;                       // kBppWarps * RP * LP
+  int* pidx_all = reinterpret_cast<int*>(lu + size_t(kBppWarps) * RP * LP);   // kBppWarps * 64
   load_hadamard(S, grams, order, mode, R);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* A = lu + size_t(warp) * RP * LP;
+  int* pidx = pidx_all + warp * 64;   // pidx[a] = index of the a-th passive variable
   constexpr int NH = (RP + 31) / 32;  // entries per lane
   double xs[NH], ys[NH], fs[NH];
   double sq2[NH];
@@ -159,23 +161,22 @@ __global__ void __launch_bounds__(kBppWarps * 32)
       const int p = __popcll(P);
       // compact passive indices: idx[a] for a < p, built identically by every lane
       // gather A (p x p) and rhs into this warp's scratch
+      // passive index list: variable r in P is the popc(P below r)-th entry
+      for (int r = lane; r < R; r += 32)
+        if ((P >> r) & 1ull) pidx[__popcll(P & ((1ull << r) - 1ull))] = r;
+      __syncwarp();
       for (int a = lane; a < p; a += 32) {
-        // a-th set bit of P
-        unsigned long long mm = P;
-        for (int t = 0; t < a; ++t) mm &= mm - 1;
-        const int ra = __ffsll(mm) - 1;
-        unsigned long long nn = P;
-        for (int b = 0; b < p; ++b) {
-          const int rb = __ffsll(nn) - 1;
-          nn &= nn - 1;
-          A[a * LP + b] = S[ra * R + rb];
-        }
+        const int ra = pidx[a];
+        for (int b = 0; b < p; ++b) A[a * LP + b] = S[ra * R + pidx[b]];
         A[a * LP + p] = fr[ra];
       }
       __syncwarp();
       bool singular = false;
       for (int cidx = 0; cidx < p; ++cidx) {
-        // pivot: max |A[i][c]| over i >= c, first index on ties (idamax)
+        // pivot: max |A[i][c]| over i >= c, first index on ties (idamax).  Exact
+        // warp argmax in three reductions: |v| >= 0 orders like its bit pattern, so
+        // max of the high words, then of the low words among those, then the
+        // smallest row index among the exact maxima.
         double bv = -1.0;
         int bi = INT_MAX;
         for (int a = cidx + lane; a < p; a += 32) {
@@ -185,14 +186,14 @@ __global__ void __launch_bounds__(kBppWarps * 32)
             bi = a;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
+        {
+          const bool cand = bi != INT_MAX;
+          const unsigned long long bits = cand ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+          const uint32_t mh = __reduce_max_sync(0xffffffffu, uint32_t(bits >> 32));
+          const uint32_t ml = __reduce_max_sync(0xffffffffu, (cand && uint32_t(bits >> 32) == mh) ? uint32_t(bits) : 0u);
+          const bool win = cand && uint32_t(bits >> 32) == mh && uint32_t(bits) == ml;
+          bi = int(__reduce_min_sync(0xffffffffu, win ? uint32_t(bi) : 0xffffffffu));
+          bv = __hiloint2double(int(mh), int(ml));
         }
         if (!(bv > 0.0)) {
           singular = true;
@@ -210,7 +211,22 @@ __global__ void __launch_bounds__(kBppWarps * 32)
         for (int a = cidx + 1 + lane; a < p; a += 32) {
           const double l = A[a * LP + cidx] * inv;
           A[a * LP + cidx] = l;
-          for (int b = cidx + 1; b <= p; ++b) A[a * LP + b] = fma(-l, A[cidx * LP + b], A[a * LP + b]);
+          double* ra = A + a * LP;
+          const double* rc = A + cidx * LP;
+          int b = cidx + 1;
+          // 8 columns per batch: all loads issued before the FMAs (same arithmetic,
+          // eight independent shared-memory round trips in flight instead of one)
+          for (; b + 8 <= p + 1; b += 8) {
+            double x[8], y[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              x[q] = rc[b + q];
+              y[q] = ra[b + q];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ra[b + q] = fma(-l, x[q], y[q]);
+          }
+          for (; b <= p; ++b) ra[b] = fma(-l, rc[b], ra[b]);
         }
         __syncwarp();
       }
@@ -443,7 +459,8 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
     if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
     NNCP_RP_CASES(rp, {
       const size_t smem = sizeof(double) * (size_t(RP) * RP + kBppWarps * 64 + RP + 1 +
-                                            size_t(kBppWarps) * RP * (RP + 1));
+                                            size_t(kBppWarps) * RP * (RP + 1)) +
+                          sizeof(int) * kBppWarps * 64;
       static bool attr = false;
       if (!attr) {
         NNCP_CUDA_TRY(cudaFuncSetAttribute(bpp_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
