@@ -55,7 +55,36 @@ __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restr
     __syncthreads();
     for (int q = threadIdx.x; q < nj; q += blockDim.x) coef[q] = coeff_value(cs, jc + q, r, R);
     __syncthreads();
-    for (int jj = warp; jj < nj; jj += 8) {
+    // U trailing indices per iteration: all 2U loads are issued before the FMAs,
+    // which run in the same (ascending jj) order as a one-at-a-time loop
+    constexpr int U = 4;
+    int jj = warp;
+    for (; jj + 8 * (U - 1) < nj; jj += 8 * U) {
+      double2 v[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double* col = tr + L * (jc + jj + 8 * u);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t l = l0 + 64 * h;
+          if (vec && l + 1 < L) {
+            v[u][h] = __ldcs(reinterpret_cast<const double2*>(col + l));
+          } else {
+            v[u][h].x = (l < L) ? __ldcs(col + l) : 0.0;
+            v[u][h].y = (l + 1 < L) ? __ldcs(col + l + 1) : 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double c = coef[jj + 8 * u];
+        acc0.x = fma(v[u][0].x, c, acc0.x);
+        acc0.y = fma(v[u][0].y, c, acc0.y);
+        acc1.x = fma(v[u][1].x, c, acc1.x);
+        acc1.y = fma(v[u][1].y, c, acc1.y);
+      }
+    }
+    for (; jj < nj; jj += 8) {
       const double c = coef[jj];
       const double* col = tr + L * (jc + jj);
 #pragma unroll
@@ -116,7 +145,19 @@ __global__ void __launch_bounds__(256) ttv_leading_kernel(const double* __restri
       const double* col = tr + L * j + lc;
       double s = 0.0;
       if (vec) {
-        for (int l = 2 * lane; l < nl; l += 64) {
+        int l = 2 * lane;
+        // 4 loads in flight, FMAs in the same order as the one-at-a-time loop
+        for (; l + 192 < nl; l += 256) {
+          double2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(col + l + 64 * u));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            s = fma(v[u].x, hc[l + 64 * u], s);
+            s = fma(v[u].y, hc[l + 64 * u + 1], s);
+          }
+        }
+        for (; l < nl; l += 64) {
           const double2 v = __ldcs(reinterpret_cast<const double2*>(col + l));
           s = fma(v.x, hc[l], s);
           s = fma(v.y, hc[l + 1], s);
