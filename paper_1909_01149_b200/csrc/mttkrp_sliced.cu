@@ -734,18 +734,23 @@ __device__ unsigned long long g_sliced_stats[1024 * 8];
 #else
 #define SLICED_WAIT(slot, bar, par) mbar_wait(bar, par)
 #endif
-template <int RP, int L>
+template <int RP, int L, int SIDE>
 struct GemmCfg {
   static constexpr int A_STAGE = TILE;                  // one digit-plane tile
   static constexpr int B_STAGE = L * RP * BK;           // all B digit rows of one k block
   static constexpr int NB = 2;
-  static constexpr int NA_FIT = (MAX_SMEM - 1024 - NB * B_STAGE) / A_STAGE;
+  // left side: the 128 x R fp64 output tile leaves through shared memory by a TMA
+  // bulk store (generic-proxy global stores of the 1 GB T_L slowed the TMA read
+  // stream by ~10%, measured)
+  static constexpr bool TMA_OUT = SIDE == NNCP_SIDE_LEFT && RP <= 32;   // fits beside >= 9 A stages
+  static constexpr int OUT_STAGE = TMA_OUT ? BM * RP * 8 : 0;
+  static constexpr int NA_FIT = (MAX_SMEM - 1024 - NB * B_STAGE - OUT_STAGE) / A_STAGE;
   static constexpr int NA = NA_FIT > 12 ? 12 : NA_FIT;
   static constexpr int ACC = L * RP;                    // TMEM columns of one accumulator set
   static constexpr int NBUF = (2 * ACC <= 512) ? 2 : 1;
   static constexpr int NEED = NBUF * ACC;
   static constexpr int TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = size_t(NB) * B_STAGE + size_t(NA) * A_STAGE + 1024;
+  static constexpr size_t SMEM = size_t(NB) * B_STAGE + size_t(NA) * A_STAGE + OUT_STAGE + 1024;
   static_assert(NA >= L, "one k block of digit tiles must fit in shared memory");
   static_assert(ACC <= 512, "accumulator does not fit in TMEM");
   static_assert(B_STAGE % 1024 == 0, "stages must keep 1 KB alignment");
@@ -762,6 +767,7 @@ struct GemmArgs {
   const int* rowexp;   // left: per output row exponent; right: nullptr (folded into B)
   const int* bexp;     // [nchunks][RP] frexp exponents of the column-chunk maxima of |B|
   double* out;         // [group][r][row]
+  int tma_out;         // left side: the output tensor map is valid (else direct stores)
   int64_t group_stride;
   int R;
 };
@@ -769,13 +775,15 @@ struct GemmArgs {
 template <int SIDE, int RP, int L>
 __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                                 const __grid_constant__ CUtensorMap mapB,
+                                                                const __grid_constant__ CUtensorMap mapO,
                                                                 GemmArgs a) {
-  using C = GemmCfg<RP, L>;
+  using C = GemmCfg<RP, L, SIDE>;
   constexpr bool LEFT = SIDE == NNCP_SIDE_LEFT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_b = smem;
   uint8_t* smem_a = smem + C::NB * C::B_STAGE;
+  double* smem_o = reinterpret_cast<double*>(smem_a + size_t(C::NA) * C::A_STAGE);   // [R][128] (left only)
   __shared__ __align__(8) uint64_t afull[C::NA], aempty[C::NA], bfull[C::NB], bempty[C::NB];
   __shared__ __align__(8) uint64_t tfull[C::NBUF], tempty[C::NBUF];
   __shared__ uint32_t tmem_base_sh;
@@ -951,7 +959,26 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
           tph ^= 1u;
         }
       }
-      if (valid) {
+      if (C::TMA_OUT && a.tma_out) {
+        // stage [r][row] in shared memory; one thread issues the TMA bulk store
+        const bool leader = threadIdx.x == 64;   // warp 2, lane 0
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // previous tile read out
+        named_bar_sync(1, 256);
+        const int rl = quad * 32 + lane;
+#pragma unroll
+        for (int r = 0; r < RH; ++r)
+          if (half * RH + r < a.R) smem_o[(half * RH + r) * BM + rl] = acc[r];
+        fence_proxy_async();
+        named_bar_sync(1, 256);
+        if (leader) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&mapO)),
+              "r"(int(tile * BM)), "r"(0), "r"(smem_u32(smem_o))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else if (valid) {
         double* o = a.out + g * a.group_stride + row;
 #pragma unroll
         for (int r = 0; r < RH; ++r)
@@ -959,6 +986,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
       }
     }
   }
+  if (C::TMA_OUT && a.tma_out && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
 #ifdef NNCP_SLICED_STATS
@@ -1024,8 +1052,9 @@ CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank
 }
 
 template <int SIDE, int RP, int L>
-int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& ga, cudaStream_t st) {
-  using C = GemmCfg<RP, L>;
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& ga,
+                cudaStream_t st) {
+  using C = GemmCfg<RP, L, SIDE>;
   static bool attr = false;
   if (!attr) {
     NNCP_CUDA_TRY(cudaFuncSetAttribute(sliced_gemm_kernel<SIDE, RP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1033,18 +1062,18 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& ga
     attr = true;
   }
   const unsigned ctas = unsigned(std::min<int64_t>(ga.items, num_sms()));
-  sliced_gemm_kernel<SIDE, RP, L><<<ctas, THREADS, C::SMEM, st>>>(ma, mb, ga);
+  sliced_gemm_kernel<SIDE, RP, L><<<ctas, THREADS, C::SMEM, st>>>(ma, mb, mo, ga);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
 
 template <int L>
-int dispatch_gemm(int side, int rp, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& ga,
-                  cudaStream_t st) {
+int dispatch_gemm(int side, int rp, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                  const GemmArgs& ga, cudaStream_t st) {
 #define NNCP_SLICED_CASE(RPV)                                                   \
   case RPV:                                                                     \
-    return side == NNCP_SIDE_LEFT ? launch_gemm<NNCP_SIDE_LEFT, RPV, L>(ma, mb, ga, st) \
-                                  : launch_gemm<NNCP_SIDE_RIGHT, RPV, L>(ma, mb, ga, st);
+    return side == NNCP_SIDE_LEFT ? launch_gemm<NNCP_SIDE_LEFT, RPV, L>(ma, mb, mo, ga, st) \
+                                  : launch_gemm<NNCP_SIDE_RIGHT, RPV, L>(ma, mb, mo, ga, st);
   switch (rp) {
     NNCP_SLICED_CASE(16)
     NNCP_SLICED_CASE(32)
@@ -1174,6 +1203,7 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
   }
 
   GemmArgs ga{};
+  int ga_tma_out = 0;
   ga.rows = p.rows;
   ga.nkb = p.Kp / BK;
   ga.kbc = p.Kc / BK;
@@ -1186,7 +1216,32 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
   ga.out = p.groups > 1 ? reinterpret_cast<double*>(w + p.part_off) : out;
   ga.group_stride = p.rows * rank;
   ga.R = rank;
-  int rc = levels == 6 ? dispatch_gemm<6>(side, p.RP, ma, mb, ga, st) : dispatch_gemm<7>(side, p.RP, ma, mb, ga, st);
+  // output map (left side: fp64 (M, R) column-major, one 128 x R box per tile; the
+  // right side stores directly and ignores it)
+  CUtensorMap mo;
+  {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(NNCP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t d[2] = {cuuint64_t(p.rows), cuuint64_t(rank)};
+    const cuuint64_t st2[1] = {cuuint64_t(p.rows) * sizeof(double)};
+    const cuuint32_t box[2] = {BM, cuuint32_t(rank)};
+    const cuuint32_t es[2] = {1, 1};
+    // TMA needs 16-byte aligned rows: odd M (or an unaligned output) takes direct stores
+    const bool ok = left && p.groups == 1 && (p.rows * sizeof(double)) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    if (ok) {
+      CUresult r = fn(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, d, st2, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(NNCP_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string(int(r)));
+    } else {
+      memset(&mo, 0, sizeof(mo));
+    }
+    ga_tma_out = ok ? 1 : 0;
+  }
+  ga.tma_out = ga_tma_out;
+  int rc = levels == 6 ? dispatch_gemm<6>(side, p.RP, ma, mb, mo, ga, st)
+                       : dispatch_gemm<7>(side, p.RP, ma, mb, mo, ga, st);
   if (rc) return rc;
   if (p.groups > 1) {
     const int64_t n = p.rows * rank;
