@@ -75,6 +75,10 @@ size_t nncp_workspace_bytes(int order, const int64_t* dims, int split, int rank)
 
 /* tensor_ops.py:76-78 norm_squared: out[0] = sum x^2 (deterministic reduction). */
 int nncp_norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
+/* Same sum (bitwise), plus out_min[0] = min x in the same pass: the negative-entry
+ * UserWarning of driver.py:571-573 without a second read of the tensor.  n >= 1. */
+int nncp_norm_squared_min(const double* x, int64_t n, double* out_sum, double* out_min, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* dimtree.py:102-127 partial_mttkrp.  dims: host.  factors: host array of `order`
  * device pointers (row-major (dims[n], R)); only the contracted side's factors are

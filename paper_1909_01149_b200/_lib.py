@@ -40,6 +40,7 @@ SIGNATURES = [
     ("nncp_choose_split", ctypes.c_int, [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("nncp_workspace_bytes", ctypes.c_size_t, [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int]),
     ("nncp_norm_squared", ctypes.c_int, [vp, ctypes.c_int64, vp, vp, ctypes.c_size_t, vp]),
+    ("nncp_norm_squared_min", ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_partial_mttkrp", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, vp, vp,
       ctypes.c_size_t, vp]),

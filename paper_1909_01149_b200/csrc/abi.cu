@@ -32,7 +32,7 @@ int normalize_gram(const double*, const double*, int64_t, int, double*, double*,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
 int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
-int norm_squared(const double*, int64_t, double*, void*, size_t, cudaStream_t);
+int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
 int status_reset(int*, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
 int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
@@ -113,7 +113,14 @@ size_t nncp_workspace_bytes(int order, const int64_t* dims, int split, int rank)
 
 int nncp_norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0) return fail(NNCP_ERR_VALUE, "negative length");
-  return norm_squared(x, n, out, ws, ws_bytes, S(stream));
+  return norm_squared(x, n, out, nullptr, ws, ws_bytes, S(stream));
+}
+
+int nncp_norm_squared_min(const double* x, int64_t n, double* out_sum, double* out_min, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (n < 1) return fail(NNCP_ERR_VALUE, "empty tensor");
+  if (!out_min) return fail(NNCP_ERR_VALUE, "null min output");
+  return norm_squared(x, n, out_sum, out_min, ws, ws_bytes, S(stream));
 }
 
 int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int split, int side,

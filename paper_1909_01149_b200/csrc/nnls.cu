@@ -380,22 +380,47 @@ __global__ void __launch_bounds__(256)
   if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, 1, out);
 }
 
+// out[0] = sum x^2 (fixed-order reduction); with out_min, also out_min[0] = min x in
+// the same pass (the reference's negative-entry warning, driver.py:571-573).
 __global__ void __launch_bounds__(512)
     norm_sq_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part, double* out,
-                   unsigned int* ticket) {
+                   double* out_min, unsigned int* ticket) {
   __shared__ double red[16];
-  double s0 = 0.0, s1 = 0.0;
+  __shared__ double redm[16];
+  double s0 = 0.0, s1 = 0.0, mn = INFINITY;
   const int64_t n2 = n / 2;
   const double2* x2 = reinterpret_cast<const double2*>(x);
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n2; e += int64_t(gridDim.x) * blockDim.x) {
     const double2 v = __ldcs(x2 + e);
     s0 = fma(v.x, v.x, s0);
     s1 = fma(v.y, v.y, s1);
+    mn = fmin(mn, fmin(v.x, v.y));
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s0 = fma(x[n - 1], x[n - 1], s0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+    s0 = fma(x[n - 1], x[n - 1], s0);
+    mn = fmin(mn, x[n - 1]);
+  }
   const double s = block_sum(s0 + s1, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
-  if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, 1, out);
+  if (out_min != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = redm[0];
+      for (int w = 1; w < int(blockDim.x >> 5); ++w) m = fmin(m, redm[w]);
+      part[gridDim.x + blockIdx.x] = m;
+    }
+  }
+  if (last_cta_ticket(ticket)) {
+    finish_partials(part, gridDim.x, 1, out);
+    if (out_min != nullptr && threadIdx.x == 0) {
+      double m = part[gridDim.x];
+      for (int b = 1; b < int(gridDim.x); ++b) m = fmin(m, part[gridDim.x + b]);
+      out_min[0] = m;
+    }
+  }
 }
 
 __global__ void status_reset_kernel(int* status) {
@@ -506,12 +531,14 @@ int inner(const double* a, const double* b, const double* lam, int64_t rows, int
   return NNCP_OK;
 }
 
-int norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+int norm_squared(const double* x, int64_t n, double* out, double* out_min, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n / 2 + 511) / 512, int64_t(num_sms()) * 8)));
-  if (w.part_elems < size_t(blocks)) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
+  if (w.part_elems < size_t(blocks) * (out_min ? 2 : 1)) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
   if (reinterpret_cast<uintptr_t>(x) % 16) return fail(NNCP_ERR_VALUE, "tensor must be 16-byte aligned");
-  norm_sq_kernel<<<blocks, 512, 0, st>>>(x, n, w.part, out, w.tickets + T_NORM);
+  if (out_min != nullptr && n < 1) return fail(NNCP_ERR_VALUE, "min of an empty tensor");
+  norm_sq_kernel<<<blocks, 512, 0, st>>>(x, n, w.part, out, out_min, w.tickets + T_NORM);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

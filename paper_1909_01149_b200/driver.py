@@ -260,7 +260,7 @@ class _Engine:
     """One execution context (one GPU, or one simulated worker) of the SPMD program."""
 
     def __init__(self, x_local: torch.Tensor, local_dims, global_dims, cfg: RunConfig, coll, layout=None,
-                 timing: bool = True):
+                 timing: bool = True, warn_negative: bool = False):
         self.x = x_local
         self.dims = tuple(int(d) for d in local_dims)
         self.global_dims = tuple(int(d) for d in global_dims)
@@ -295,7 +295,9 @@ class _Engine:
         self.grams = torch.zeros((N, R, R), **f64)
         self.lam = torch.ones(R, **f64)
         self.nsq = torch.zeros(R, **f64)
-        self.scal = torch.zeros(4, **f64)           # beta, gamma, alpha, beta0
+        self.scal = torch.zeros(5, **f64)           # beta, gamma, alpha, beta0, min x (warn_negative)
+        # driver.py:571-573: the negative-entry warning, from the initial norm pass
+        self.warn_negative = bool(warn_negative) and cfg.algorithm != "ucp"
         self.status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32, device=dev)
         self.mbar = torch.empty((max(self.dims), R), **f64)
         self.hhat = torch.empty((max(max(self.n_owned), 1), R), **f64)
@@ -339,13 +341,20 @@ class _Engine:
         self.report.begin_row()
         wall0 = time.perf_counter()
         self.timer.start()
-        _lib.check(lib.nncp_norm_squared(_lib.ptr(self.x), self.x.numel(), _lib.vp(self.scal.data_ptr() + 16),
-                                         self.ws.ptr, self.ws.nbytes, st))
+        if self.warn_negative:
+            _lib.check(lib.nncp_norm_squared_min(_lib.ptr(self.x), self.x.numel(),
+                                                 _lib.vp(self.scal.data_ptr() + 16),
+                                                 _lib.vp(self.scal.data_ptr() + 32), self.ws.ptr, self.ws.nbytes, st))
+        else:
+            _lib.check(lib.nncp_norm_squared(_lib.ptr(self.x), self.x.numel(), _lib.vp(self.scal.data_ptr() + 16),
+                                             self.ws.ptr, self.ws.nbytes, st))
         self.timer.mark("Error")
         alpha_t = self.scal[2:3]
         self.coll.all_reduce(alpha_t)
         self.timer.mark("AllReduce")
         self.alpha = float(alpha_t.item())
+        if self.warn_negative and float(self.scal[4].item()) < 0.0:
+            warnings.warn("tensor has negative entries; nonnegative model will not fit")
         if self.alpha <= 0.0:
             raise ValueError("zero tensor has no relative error")
         cfg = self.cfg
@@ -619,9 +628,10 @@ def _warn_if_negative(x: DenseTensor, cfg: RunConfig):
 
 
 def run_local(x_local: torch.Tensor, local_dims, global_dims, cfg: RunConfig, coll=None, layout=None,
-              timing: bool = True):
+              timing: bool = True, warn_negative: bool = False):
     """Run the SPMD program on one execution context; returns (engine, report)."""
-    eng = _Engine(x_local, local_dims, global_dims, cfg, coll or IdentityCollectives(), layout, timing)
+    eng = _Engine(x_local, local_dims, global_dims, cfg, coll or IdentityCollectives(), layout, timing,
+                  warn_negative=warn_negative)
     eng.initialise()
     eng.iterate()
     eng.report.counters = eng.coll.counters
@@ -634,8 +644,8 @@ def nncp_sequential(x: DenseTensor, cfg: RunConfig) -> RunReport:
     if cfg.grid is not None and int(np.prod(cfg.grid)) != 1:
         raise ValueError("sequential driver got a nontrivial grid; use nncp_parallel")
     xd = x.to_device()
-    _warn_if_negative(xd, cfg)
-    eng, rep = run_local(xd.data, x.dims, x.dims, cfg)
+    # the negative-entry warning comes from the engine's first pass over the tensor
+    eng, rep = run_local(xd.data, x.dims, x.dims, cfg, warn_negative=True)
     owned, lam = eng.model_host()
     rep.model = FactorSet(owned, lam)
     return rep
