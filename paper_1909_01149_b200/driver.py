@@ -235,8 +235,9 @@ SLICED_MIN_ELEMS = 1 << 22       # below this the fp64 path's fewer launches win
 SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
 # partial-MTTKRP cost model for mttkrp_kernel="auto" (B200 measurements):
 # FP64 DMMA path reaches ~87% of max(8 I / BW, 2 I R / 37.1 TF); the sliced path streams
-# 6 I bytes at ~6.9 TB/s plus ~90 us of per-call digit prep and launches
-_HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 9e-5
+# 6 I bytes at ~6.9 TB/s plus ~50 us of per-call digit prep, launches and tail
+# (512^3 R=16: 0.155 / 0.176 ms sliced vs 0.196 / 0.185 ms DMMA)
+_HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 5e-5
 
 
 def _use_sliced(kind: str, dims, split: int, rank: int, dev) -> bool:
