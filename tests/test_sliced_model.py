@@ -13,7 +13,8 @@ MTTKRP_TOL = 1e-12
 
 CASES = [((7, 9, 11), 5), ((33, 17, 5), 1), ((96, 64, 48), 20), ((256, 130, 40), 8), ((128, 24, 30, 8), 12),
          ((20, 18, 16, 14), 33), ((256, 256, 64), 8), ((40, 40, 20000), 4),
-         ((128, 16, 16, 200), 4)]   # split 3: right side = 3 Khatri-Rao factors, segment-reuse path
+         ((128, 16, 16, 200), 4),   # split 3: right side = 3 Khatri-Rao factors, segment-reuse path
+         ((300, 260, 90), 64), ((256, 128, 96), 50)]   # RP = 64
 
 
 def _case(dims, r, signed=False):
