@@ -71,6 +71,9 @@ class RunConfig:
     # (DESIGN.md §4.4), "fp64" = FP64 DMMA, "auto" = sliced when its cost model wins
     # and the slices fit in HBM
     mttkrp_kernel: str = "auto"
+    # digit levels of the sliced engine: 6 (46-bit operands, 6 B/element) or 7 (54-bit,
+    # for rows spanning extreme dynamic ranges; 7 B/element)
+    mttkrp_levels: int = 6
 
     def validate(self, order: int):
         if self.rank < 1:
@@ -91,6 +94,8 @@ class RunConfig:
                 f"(supported: {', '.join(IN_SCOPE_ALGORITHMS)})")
         if self.mttkrp_kernel not in ("auto", "sliced", "fp64"):
             raise ValueError(f"unknown mttkrp_kernel {self.mttkrp_kernel!r} (auto, sliced, fp64)")
+        if self.mttkrp_levels not in (6, 7):
+            raise ValueError(f"mttkrp_levels must be 6 or 7, got {self.mttkrp_levels!r}")
         if self.rank > _lib.MAX_RANK:
             raise NotImplementedError(f"rank {self.rank} exceeds the device limit {_lib.MAX_RANK}")
         if order > _lib.MAX_ORDER:
@@ -240,7 +245,7 @@ SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
 _HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 5e-5
 
 
-def _use_sliced(kind: str, dims, split: int, rank: int, dev) -> bool:
+def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6) -> bool:
     """Resolve RunConfig.mttkrp_kernel for one execution context."""
     if kind == "fp64":
         return False
@@ -250,11 +255,11 @@ def _use_sliced(kind: str, dims, split: int, rank: int, dev) -> bool:
     if size < SLICED_MIN_ELEMS:
         return False
     t_fp64 = max(8.0 * size / _HBM_BPS, 2.0 * size * rank / _DMMA_FLOPS) / 0.87
-    t_sliced = 6.0 * size / _SLICED_BPS + _SLICED_FIXED_S
+    t_sliced = float(levels) * size / _SLICED_BPS + _SLICED_FIXED_S
     if t_sliced >= t_fp64:
         return False
     free, _ = torch.cuda.mem_get_info(dev)
-    return SlicedTensor.nbytes(dims, split) + SLICED_HBM_MARGIN <= free
+    return SlicedTensor.nbytes(dims, split, levels) + SLICED_HBM_MARGIN <= free
 
 
 class _Engine:
@@ -284,8 +289,8 @@ class _Engine:
         self.n_owned = [s.stop - s.start for s in self.owned_rows]
         self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
         self.sliced = None
-        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, self.R, dev):
-            self.sliced = SlicedTensor(x_local, self.dims, self.plan.split)
+        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, self.R, dev, cfg.mttkrp_levels):
+            self.sliced = SlicedTensor(x_local, self.dims, self.plan.split, cfg.mttkrp_levels)
         ws_bytes = self.plan.workspace_bytes()
         if self.sliced is not None:
             ws_bytes = max(ws_bytes, self.plan.sliced_workspace_bytes(self.sliced.levels))

@@ -209,3 +209,19 @@ def test_sliced_grid_runs_vs_golden(P, golden):
         assert np.max(np.abs(np.array(par.errors) - g[f"{tag}_errors"])) <= TRACE_TOL, tag
         for n in range(len(dims)):
             assert np.max(np.abs(par.model.factors[n] - g[f"{tag}_f{n}"])) <= FACTOR_TOL, (tag, n)
+
+
+def test_sliced_seven_levels_run(P):
+    """RunConfig.mttkrp_levels=7 (54-bit digit operands) through the whole driver."""
+    rng = np.random.default_rng(21)
+    dims, r = (96, 80, 64), 12
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    errors, factors, _, _, _ = O.run_sequential(x, dims, r, "hals", 5, 0.0, 0)
+    cfg = P.RunConfig(rank=r, algorithm="hals", max_iters=5, tol=0.0, mttkrp_kernel="sliced", mttkrp_levels=7)
+    rep = P.nncp_sequential(P.DenseTensor(dims, x), cfg)
+    assert np.max(np.abs(np.array(rep.errors) - np.array(errors))) <= TRACE_TOL
+    for a, b in zip(rep.model.factors, factors):
+        assert np.max(np.abs(a - b)) <= FACTOR_TOL
+    with pytest.raises(ValueError, match="mttkrp_levels"):
+        P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, mttkrp_levels=5))

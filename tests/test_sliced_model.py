@@ -27,7 +27,11 @@ def _case(dims, r, signed=False):
     return x, hs
 
 
-@pytest.mark.parametrize("dims,r", CASES)
+# the CPU model runs exact int64 matmuls in numpy: keep the CPU suite to the smaller cases
+CPU_CASES = [c for c in CASES if np.prod(c[0]) * c[1] <= 3e7]
+
+
+@pytest.mark.parametrize("dims,r", CPU_CASES)
 def test_model_matches_oracle(dims, r):
     x, hs = _case(dims, r)
     from paper_1909_01149_b200.dimtree import choose_split_mode
