@@ -104,6 +104,18 @@ int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dim
                                const double* const* factors, int rank, int levels, double* out, void* ws,
                                size_t ws_bytes, void* stream);
 
+/* The left sliced partial plus the dimension tree's first trailing multi-TTV in one
+ * pass (dimtree.py:241-250 mode 1: out_trailing = multi_ttv(T_L, H_2, trailing)),
+ * accumulated in the GEMM epilogue instead of re-reading T_L.  Supported for split 2,
+ * dims[0] a multiple of 128, rank <= 32 and long row tiles (nncp_sliced_trailing_supported);
+ * NNCP_ERR_UNSUPPORTED otherwise (use nncp_partial_mttkrp_sliced + nncp_multi_ttv).  out_temp as for the left partial;
+ * out_trailing: column-major (dims[0], R). */
+/* 1 when nncp_partial_mttkrp_sliced_trailing supports (and is worth it for) this shape. */
+int nncp_sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels);
+int nncp_partial_mttkrp_sliced_trailing(const void* sliced, int order, const int64_t* dims, int split,
+                                        const double* const* factors, int rank, int levels, double* out_temp,
+                                        double* out_trailing, void* ws, size_t ws_bytes, void* stream);
+
 /* dimtree.py:135-175 multi_ttv.  temp: column-major (prod(ret_dims), R).
  * TRAILING: coeff = KRP(coeff[0..ncoeff)) with coeff_rows[k] rows each, whose
  *   product must equal prod(ret_dims[1:]); out retains ret_dims[0].

@@ -53,6 +53,11 @@ SIGNATURES = [
     ("nncp_partial_mttkrp_sliced", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, vp,
       vp, ctypes.c_size_t, vp]),
+    ("nncp_sliced_trailing_supported", ctypes.c_int,
+     [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("nncp_partial_mttkrp_sliced_trailing", ctypes.c_int,
+     [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, vp, vp, vp,
+      ctypes.c_size_t, vp]),
     ("nncp_multi_ttv", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), c_i64p, ctypes.c_int, vp, vp]),
     ("nncp_temp_to_rows", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp]),

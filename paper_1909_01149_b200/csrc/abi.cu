@@ -51,9 +51,10 @@ int synthetic(double*, int, const int64_t*, const int64_t*, const int64_t*, cons
 
 size_t sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels);
 size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int levels);
+bool sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels);
 int slice_tensor(const double*, int, const int64_t*, int, int, void*, size_t, cudaStream_t);
-int sliced_partial_mttkrp(const void*, int, const int64_t*, int, int, const double* const*, int, int, double*, void*,
-                          size_t, cudaStream_t);
+int sliced_partial_mttkrp(const void*, int, const int64_t*, int, int, const double* const*, int, int, double*, double*,
+                          void*, size_t, cudaStream_t);
 
 // caller buffers for the sliced path are used from the next 1 KB boundary on
 static inline void* align1k(const void* p, size_t bytes, size_t* avail) {
@@ -174,7 +175,30 @@ int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dim
   const void* base = align1k(sliced, 1024, &dummy);
   // the first 256 workspace bytes hold the reduction tickets of the other kernels
   void* w = (ws && ws_bytes > 256) ? align1k(static_cast<char*>(ws) + 256, ws_bytes - 256, &avail) : nullptr;
-  return sliced_partial_mttkrp(base, order, dims, split, side, factors, rank, levels, out, w, avail, S(stream));
+  return sliced_partial_mttkrp(base, order, dims, split, side, factors, rank, levels, out, nullptr, w, avail,
+                               S(stream));
+}
+
+int nncp_sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels) {
+  if (order < 2 || order > kMaxOrder || rank < 1 || rank > kMaxRank || split < 1 || split >= order) return 0;
+  for (int n = 0; n < order; ++n)
+    if (dims[n] < 1) return 0;
+  if (levels != 6 && levels != 7) return 0;
+  return sliced_trailing_supported(order, dims, split, rank, levels) ? 1 : 0;
+}
+
+int nncp_partial_mttkrp_sliced_trailing(const void* sliced, int order, const int64_t* dims, int split,
+                                        const double* const* factors, int rank, int levels, double* out_temp,
+                                        double* out_trailing, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_common(order, dims, rank);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (!sliced || !out_trailing) return fail(NNCP_ERR_VALUE, "null sliced tensor or trailing output");
+  size_t dummy = 0, avail = 0;
+  const void* base = align1k(sliced, 1024, &dummy);
+  void* w = (ws && ws_bytes > 256) ? align1k(static_cast<char*>(ws) + 256, ws_bytes - 256, &avail) : nullptr;
+  return sliced_partial_mttkrp(base, order, dims, split, NNCP_SIDE_LEFT, factors, rank, levels, out_temp,
+                               out_trailing, w, avail, S(stream));
 }
 
 int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, int side,

@@ -629,6 +629,30 @@ int dispatch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cud
   }
 }
 
+// out1[i1 + I1 r] = sum over the CTAs whose contiguous item range touched i1's block
+// of their partials, in CTA order (deterministic).  Items are ib * O + o.
+__global__ void ttv_partials_reduce_kernel(const double* __restrict__ tpart, int64_t items, int ctas, int64_t nout,
+                                           int64_t slots, int64_t I1, int R, int RP, double* __restrict__ out1) {
+  const int64_t n = I1 * R;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i1 = e % I1, r = e / I1;
+    const int64_t ib = i1 / 128, row = i1 % 128;
+    // CTAs c with [c items / ctas, (c+1) items / ctas) overlapping [ib O, (ib+1) O)
+    int64_t c_lo = (ib * nout * ctas) / items;
+    while (c_lo > 0 && (c_lo * items) / ctas > ib * nout) --c_lo;
+    while (c_lo < ctas - 1 && ((c_lo + 1) * items) / ctas <= ib * nout) ++c_lo;
+    double s = 0.0;
+    for (int64_t c = c_lo; c < ctas; ++c) {
+      const int64_t b = c * items / ctas, en = (c + 1) * items / ctas;
+      if (b >= (ib + 1) * nout) break;
+      if (en <= b) continue;
+      const int64_t ib0 = b / nout;
+      s += tpart[((c * slots + (ib - ib0)) * 128 + row) * RP + r];
+    }
+    out1[e] = s;
+  }
+}
+
 __global__ void group_reduce_kernel(const double* __restrict__ part, int groups, int64_t stride, int64_t n,
                                     double* __restrict__ out) {
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
@@ -770,7 +794,40 @@ struct GemmArgs {
   int tma_out;         // left side: the output tensor map is valid (else direct stores)
   int64_t group_stride;
   int R;
+  // fused trailing multi-TTV (left side, split S = 2, dims[0] % 128 == 0, RP <= 32):
+  // the epilogue also accumulates out1[i1, r] = sum_o T_L[i1 + I1 o, r] H_1[o, r]
+  // (dimtree.py:159-165); tiles visited i1-block-major in contiguous per-CTA ranges,
+  // per-CTA partials [cta][slot][128][RP] reduced in CTA order afterwards
+  int fuse;
+  int64_t nib, nout;   // i1 blocks (I1 / 128) and outer indices (M / I1)
+  const double* cf[1];  // the trailing factor H_1 (split S = 2)
+  double* tpart;
+  int64_t slots;       // partial slots per CTA
 };
+
+// Items of one CTA: round-robin over CTAs, or (fused TTV) one contiguous range.
+__device__ __forceinline__ void item_range(const GemmArgs& a, int64_t& b, int64_t& e, int64_t& step) {
+  if (a.fuse) {
+    b = int64_t(blockIdx.x) * a.items / gridDim.x;
+    e = int64_t(blockIdx.x + 1) * a.items / gridDim.x;
+    step = 1;
+  } else {
+    b = blockIdx.x;
+    e = a.items;
+    step = gridDim.x;
+  }
+}
+
+// item -> (row tile, split-K group)
+__device__ __forceinline__ void item_tile(const GemmArgs& a, int64_t it, int64_t& tile, int64_t& g) {
+  if (a.fuse) {
+    tile = it / a.nout + a.nib * (it % a.nout);   // item = ib * O + o  ->  m block = ib + nib * o
+    g = 0;
+  } else {
+    tile = it % a.row_tiles;
+    g = it / a.row_tiles;
+  }
+}
 
 template <int SIDE, int RP, int L>
 __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -827,8 +884,11 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
       const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
       int as = 0, bsx = 0;
       uint32_t aph = 0, bph = 0;
-      for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
-        const int64_t tile = it % a.row_tiles, g = it / a.row_tiles;
+      int64_t it_b, it_e, it_s;
+      item_range(a, it_b, it_e, it_s);
+      for (int64_t it = it_b; it < it_e; it += it_s) {
+        int64_t tile, g;
+        item_tile(a, it, tile, g);
         const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
         for (int64_t kb = c0 * a.kbc, kend = min(a.nkb, c1 * a.kbc); kb < kend; ++kb) {
           SLICED_WAIT(0, &bempty[bsx], bph ^ 1u);
@@ -860,8 +920,11 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
       // ------------------------------------------------ MMA issuer ------
       int as = 0, bsx = 0, abuf = 0;
       uint32_t aph = 0, bph = 0, tph = 0;
-      for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
-        const int64_t g = it / a.row_tiles;
+      int64_t it_b, it_e, it_s;
+      item_range(a, it_b, it_e, it_s);
+      for (int64_t it = it_b; it < it_e; it += it_s) {
+        int64_t tile, g;
+        item_tile(a, it, tile, g);
         const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
         for (int64_t c = c0; c < c1; ++c) {
           SLICED_WAIT(2, &tempty[abuf], tph ^ 1u);
@@ -918,8 +981,24 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
     const int quad = warp & 3, half = (warp - 2) >> 2;
     int abuf = 0;
     uint32_t tph = 0;
-    for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
-      const int64_t tile = it % a.row_tiles, g = it / a.row_tiles;
+    int64_t it_b, it_e, it_s;
+    item_range(a, it_b, it_e, it_s);
+    // fused trailing TTV state: partial sums of this CTA's current i1 block (RP <= 32:
+    // the extra RH registers would spill the RP = 64 epilogue)
+    constexpr bool FUSE_OK = LEFT && RP <= 32;
+    double fz[RH];
+#pragma unroll
+    for (int r = 0; r < RH; ++r) fz[r] = 0.0;
+    int64_t cur_ib = -1;
+    const int64_t ib0 = a.fuse ? it_b / a.nout : 0;
+    auto flush_ttv = [&](int64_t ib) {
+      double* dst = a.tpart + ((int64_t(blockIdx.x) * a.slots + (ib - ib0)) * BM + quad * 32 + lane) * RP + half * RH;
+#pragma unroll
+      for (int r = 0; r < RH; ++r) dst[r] = fz[r];
+    };
+    for (int64_t it = it_b; it < it_e; it += it_s) {
+      int64_t tile, g;
+      item_tile(a, it, tile, g);
       const int64_t c0 = g * a.nchunks / a.groups, c1 = (g + 1) * a.nchunks / a.groups;
       const int64_t row = tile * BM + quad * 32 + lane;
       const bool valid = row < a.rows;
@@ -959,6 +1038,22 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
           tph ^= 1u;
         }
       }
+      if (FUSE_OK && a.fuse) {
+        const int64_t ib = it / a.nout, o = it % a.nout;
+        if (ib != cur_ib) {
+          if (cur_ib >= 0) flush_ttv(cur_ib);
+#pragma unroll
+          for (int r = 0; r < RH; ++r) fz[r] = 0.0;
+          cur_ib = ib;
+        }
+        // C[o, r] = H_1[o, r] (split S = 2: one trailing factor)
+        const double* crow = a.cf[0] + o * a.R;
+#pragma unroll
+        for (int r = 0; r < RH; ++r) {
+          const int col = half * RH + r;
+          fz[r] = fma(acc[r], col < a.R ? __ldg(crow + col) : 0.0, fz[r]);
+        }
+      }
       if (C::TMA_OUT && a.tma_out) {
         // stage [r][row] in shared memory; one thread issues the TMA bulk store
         const bool leader = threadIdx.x == 64;   // warp 2, lane 0
@@ -985,6 +1080,7 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
           if (half * RH + r < a.R) __stcs(o + int64_t(half * RH + r) * a.rows, acc[r]);   // streaming store
       }
     }
+    if (FUSE_OK && a.fuse && cur_ib >= 0) flush_ttv(cur_ib);
   }
   if (C::TMA_OUT && a.tma_out && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
@@ -1017,6 +1113,9 @@ struct CallPlan {
   int64_t K, Kp, Kc, nchunks, rows, row_tiles;
   int groups;
   size_t bexp_off, bs_off, part_off, ws_bytes;
+  // fused trailing TTV (left side): eligible, CTAs, partial slots per CTA, I1, outer count
+  bool fuse;
+  int64_t fctas, fslots, I1, nout;
 };
 
 CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank, int L) {
@@ -1048,6 +1147,20 @@ CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank
   p.bs_off = size_t(align_up(p.nchunks * p.RP * 4, 1024));
   p.part_off = p.bs_off + size_t(align_up(int64_t(L) * p.RP * p.Kp, 1024));
   p.ws_bytes = p.part_off + (p.groups > 1 ? size_t(p.groups) * p.rows * rank * sizeof(double) : 0);
+  // fused trailing TTV: split 2, whole 128-row blocks of the first mode, RP <= 32, and
+  // long row tiles in long per-CTA ranges (measured: with 2-block tiles (c4) the extra
+  // epilogue work and the scattered i1-block-major order cost what the TTV saves;
+  // with ~3 tiles per CTA (c3) the temporary is too small to matter)
+  p.I1 = dims[0];
+  p.fuse = left && split == 2 && order >= 3 && dims[0] % BM == 0 && p.RP <= 32 && p.Kp / BK >= 8 &&
+           p.row_tiles >= 16 * sms;
+  if (p.fuse) {
+    p.nout = p.t.M / p.I1;
+    p.fctas = std::min<int64_t>(p.row_tiles, sms);
+    const int64_t per = (p.row_tiles + p.fctas - 1) / p.fctas;
+    p.fslots = (per + p.nout - 1) / p.nout + 1;
+    p.ws_bytes = std::max(p.ws_bytes, p.part_off + size_t(p.fctas) * p.fslots * BM * p.RP * sizeof(double));
+  }
   return p;
 }
 
@@ -1097,6 +1210,10 @@ size_t sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels
   return sliced::tensor_layout(order, dims, split, levels).total;
 }
 
+bool sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels) {
+  return sliced::plan_call(order, dims, split, NNCP_SIDE_LEFT, rank, levels).fuse;
+}
+
 size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int levels) {
   const auto l = sliced::plan_call(order, dims, split, NNCP_SIDE_LEFT, rank, levels);
   const auto r = sliced::plan_call(order, dims, split, NNCP_SIDE_RIGHT, rank, levels);
@@ -1143,8 +1260,8 @@ int slice_tensor(const double* x, int order, const int64_t* dims, int split, int
 }
 
 int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, int split, int side,
-                          const double* const* factors, int rank, int levels, double* out, void* ws,
-                          size_t ws_bytes, cudaStream_t st) {
+                          const double* const* factors, int rank, int levels, double* out, double* out_trailing,
+                          void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace sliced;
   if (int rc = check_levels(levels)) return rc;
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP: rank outside [1, 64]");
@@ -1152,6 +1269,8 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
   if (ws == nullptr || ws_bytes < p.ws_bytes) return fail(NNCP_ERR_VALUE, "workspace too small for sliced MTTKRP");
   if (reinterpret_cast<uintptr_t>(ws) % 1024) return fail(NNCP_ERR_VALUE, "workspace must be 1 KB aligned");
   const bool left = side == NNCP_SIDE_LEFT;
+  if (out_trailing != nullptr && !p.fuse)
+    return fail(NNCP_ERR_UNSUPPORTED, "fused trailing TTV needs the left side, split 2, dims[0] % 128 == 0, rank <= 32");
   const uint8_t* base = static_cast<const uint8_t*>(sliced_x);
   const int* rowexp = reinterpret_cast<const int*>(base);
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -1240,6 +1359,15 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
     ga_tma_out = ok ? 1 : 0;
   }
   ga.tma_out = ga_tma_out;
+  if (out_trailing != nullptr) {
+    if (!factors[1]) return fail(NNCP_ERR_VALUE, "null factor pointer for the trailing TTV");
+    ga.fuse = 1;
+    ga.nib = p.I1 / BM;
+    ga.nout = p.nout;
+    ga.cf[0] = factors[1];
+    ga.tpart = reinterpret_cast<double*>(w + p.part_off);
+    ga.slots = p.fslots;
+  }
   int rc = levels == 6 ? dispatch_gemm<6>(side, p.RP, ma, mb, mo, ga, st)
                        : dispatch_gemm<7>(side, p.RP, ma, mb, mo, ga, st);
   if (rc) return rc;
@@ -1247,6 +1375,13 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
     const int64_t n = p.rows * rank;
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
     group_reduce_kernel<<<blocks, 256, 0, st>>>(ga.out, p.groups, n, n, out);
+    NNCP_LAUNCH_CHECK();
+  }
+  if (out_trailing != nullptr) {
+    const int64_t n = p.I1 * rank;
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    ttv_partials_reduce_kernel<<<blocks, 256, 0, st>>>(ga.tpart, ga.items, int(p.fctas), p.nout, p.fslots, p.I1,
+                                                       rank, p.RP, out_trailing);
     NNCP_LAUNCH_CHECK();
   }
   return NNCP_OK;

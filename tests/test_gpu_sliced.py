@@ -225,3 +225,30 @@ def test_sliced_seven_levels_run(P):
         assert np.max(np.abs(a - b)) <= FACTOR_TOL
     with pytest.raises(ValueError, match="mttkrp_levels"):
         P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, mttkrp_levels=5))
+
+
+@pytest.mark.parametrize("dims,r", [((1024, 300, 1024), 32), ((512, 600, 32, 32), 24), ((768, 400, 1030), 1)])
+def test_fused_trailing_ttv(P, dims, r):
+    """Left partial + first trailing TTV in one sliced pass == partial then multi_ttv (T_L bitwise, the
+    mode-1 MTTKRP to 1e-12), and the mode-1 MTTKRP vs the oracle."""
+    import torch
+
+    from paper_1909_01149_b200.dimtree import fused_trailing_ok, partial_mttkrp_trailing
+
+    rng = np.random.default_rng(sum(dims) * r)
+    x = rng.random(int(np.prod(dims)))
+    hs = [rng.random((d, r)) for d in dims]
+    plan = P.DimTreePlan.create(dims, r)
+    xd = P.DenseTensor(dims, x).to_device()
+    sl = _sliced(P, xd, plan)
+    assert fused_trailing_ok(plan, sl)
+    ws = P.tensor_ops.Workspace(max(plan.workspace_bytes(), plan.sliced_workspace_bytes()))
+    t_ref = P.partial_mttkrp(xd, hs, "left", plan, workspace=ws, sliced=sl).data.clone()
+    m_ref = P.multi_ttv(P.dimtree.TempTensor(dims[:2], r, t_ref), hs[1:2], "trailing").data.clone()
+    out_t = torch.empty_like(t_ref)
+    out_m = torch.empty(dims[0] * r, dtype=torch.float64, device="cuda")
+    partial_mttkrp_trailing(xd, hs, plan, sl, out_t, out_m, ws)
+    assert torch.equal(out_t, t_ref)
+    assert float(torch.linalg.norm(out_m - m_ref) / torch.linalg.norm(m_ref)) <= MTTKRP_TOL
+    want = O.naive_mttkrp(x, dims, hs, 0)
+    assert rel_fro(_np(out_m.view(r, dims[0]).T), want) <= MTTKRP_TOL
