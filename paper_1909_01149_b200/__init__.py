@@ -7,8 +7,8 @@ Gram-trick error and the N-d grid.  All numerics run in libnncp_b200.so
 (sm_100a); there is no CPU fallback.
 """
 
-from .dimtree import (DimTreeContext, DimTreePlan, TempTensor, choose_split_mode, multi_ttv,  # noqa: F401
-                      partial_mttkrp)
+from .dimtree import (DimTreeContext, DimTreePlan, TempTensor, choose_balanced_split,  # noqa: F401
+                      choose_split_mode, multi_ttv, partial_mttkrp)
 from .driver import (ALGORITHMS, CATEGORIES, IN_SCOPE_ALGORITHMS, RunConfig, RunReport, init_factor,  # noqa: F401
                      nncp_parallel, nncp_sequential, record_category, relative_error, run_local)
 from .grid import CommCounters, DistMap, Grid, block_partition  # noqa: F401

@@ -1128,13 +1128,15 @@ CallPlan plan_call(int order, const int64_t* dims, int split, int side, int rank
   p.rows = left ? p.t.M : p.t.J;
   p.row_tiles = left ? p.t.nmb : p.t.njb;
   const int64_t sms = num_sms();
-  if (left) {
+  if (left && p.row_tiles >= sms) {
     p.groups = 1;
     p.Kc = std::min<int64_t>(KC_MAX, align_up(p.Kp, 256));
   } else {
     // split the contraction into groups so row_tiles x groups fills the SMs; the
     // row tiles of a group stream the same B chunks at the same time (L2 reuse)
     // Chunk length chosen so every group gets the same number of chunks (q).
+    // (Either side: the left one has few row tiles under a balanced split, e.g.
+    // 4096 x (2048 * 256).)
     const int64_t want = std::max<int64_t>(1, sms / p.row_tiles);
     const int64_t per_group = (p.Kp + want - 1) / want;
     const int64_t q = std::max<int64_t>(1, (per_group + KC_MAX - 1) / KC_MAX);

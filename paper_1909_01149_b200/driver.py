@@ -21,6 +21,7 @@ Category seconds come from CUDA events on the launching stream.
 
 from __future__ import annotations
 
+import math
 import threading
 import time
 import warnings
@@ -30,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dimtree import DimTreeContext, DimTreePlan, SlicedTensor
+from .dimtree import DimTreeContext, DimTreePlan, SlicedTensor, choose_balanced_split
 from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, RankLayout, ThreadCollectives,
                    ThreadGrid, block_partition)
 from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
@@ -74,6 +75,10 @@ class RunConfig:
     # digit levels of the sliced engine: 6 (46-bit operands, 6 B/element) or 7 (54-bit,
     # for rows spanning extreme dynamic ranges; 7 B/element)
     mttkrp_levels: int = 6
+    # dimension-tree root split: "reference" = the reference rule (first S with
+    # M >= J, dimtree.py:25-39); "auto" = that rule, except that the sliced engine
+    # takes the split minimising M + J when it at least halves it
+    dimtree_split: str = "auto"
 
     def validate(self, order: int):
         if self.rank < 1:
@@ -94,6 +99,8 @@ class RunConfig:
                 f"(supported: {', '.join(IN_SCOPE_ALGORITHMS)})")
         if self.mttkrp_kernel not in ("auto", "sliced", "fp64"):
             raise ValueError(f"unknown mttkrp_kernel {self.mttkrp_kernel!r} (auto, sliced, fp64)")
+        if self.dimtree_split not in ("auto", "reference"):
+            raise ValueError(f"unknown dimtree_split {self.dimtree_split!r} (auto, reference)")
         if self.mttkrp_levels not in (6, 7):
             raise ValueError(f"mttkrp_levels must be 6 or 7, got {self.mttkrp_levels!r}")
         if self.rank > _lib.MAX_RANK:
@@ -262,6 +269,11 @@ def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6) ->
     return SlicedTensor.nbytes(dims, split, levels) + SLICED_HBM_MARGIN <= free
 
 
+def _split_rows(dims, s: int) -> int:
+    """M + J of the root split S: the rows of the two partial outputs and of the Khatri-Rao digit sides."""
+    return math.prod(dims[:s]) + math.prod(dims[s:])
+
+
 class _Engine:
     """One execution context (one GPU, or one simulated worker) of the SPMD program."""
 
@@ -290,6 +302,10 @@ class _Engine:
         self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
         self.sliced = None
         if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, self.R, dev, cfg.mttkrp_levels):
+            if cfg.dimtree_split == "auto":
+                s_bal = choose_balanced_split(self.dims)
+                if 2 * _split_rows(self.dims, s_bal) <= _split_rows(self.dims, self.plan.split):
+                    self.plan = DimTreePlan(self.dims, self.R, s_bal)
             self.sliced = SlicedTensor(x_local, self.dims, self.plan.split, cfg.mttkrp_levels)
         ws_bytes = self.plan.workspace_bytes()
         if self.sliced is not None:

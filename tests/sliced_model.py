@@ -57,7 +57,7 @@ def plan(dims, split, side, rank, sms=148):
     k, kp = (j, jp) if left else (m, mp)
     rows = m if left else j
     row_tiles = (mp if left else jp) // BM
-    if left:
+    if left and row_tiles >= sms:
         groups = 1
         kc = min(KC_MAX, _align(kp, 256))
     else:

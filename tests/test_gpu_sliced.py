@@ -252,3 +252,24 @@ def test_fused_trailing_ttv(P, dims, r):
     assert float(torch.linalg.norm(out_m - m_ref) / torch.linalg.norm(m_ref)) <= MTTKRP_TOL
     want = O.naive_mttkrp(x, dims, hs, 0)
     assert rel_fro(_np(out_m.view(r, dims[0]).T), want) <= MTTKRP_TOL
+
+
+def test_sliced_balanced_split_run(P):
+    """dimtree_split="auto": the sliced engine takes the split minimising M + J (4096 x 2048 x 256-like
+    shapes: S = 1 instead of the reference's S = 2); same traces as the oracle and as the reference split."""
+    rng = np.random.default_rng(31)
+    dims, r = (192, 96, 24), 12
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    errors, factors, _, _, _ = O.run_sequential(x, dims, r, "hals", 6, 0.0, 0)
+    reps = {}
+    for mode in ("auto", "reference"):
+        cfg = P.RunConfig(rank=r, algorithm="hals", max_iters=6, tol=0.0, mttkrp_kernel="sliced", dimtree_split=mode)
+        reps[mode] = P.nncp_sequential(P.DenseTensor(dims, x), cfg)
+    assert reps["auto"].split_mode == 1 and reps["reference"].split_mode == 2
+    for rep in reps.values():
+        assert np.max(np.abs(np.array(rep.errors) - np.array(errors))) <= TRACE_TOL
+        for a, b in zip(rep.model.factors, factors):
+            assert np.max(np.abs(a - b)) <= FACTOR_TOL
+    with pytest.raises(ValueError, match="dimtree_split"):
+        P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, dimtree_split="middle"))
