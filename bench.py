@@ -74,6 +74,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = 0
 
     def start(self):
         try:
@@ -84,6 +85,15 @@ class ClockSampler:
             self.thread.start()
         except Exception:  # noqa: BLE001
             self.proc = None
+
+    def mark(self):
+        """Start of the timed region: samples from here on count.  (nvidia-smi is started
+        before the warm-up: its NVML start-up inside the timed region cost up to ~2 ms per
+        2048^3 step, measured.)"""
+        t_end = time.perf_counter() + 3.0
+        while self.proc is not None and not self.lines and time.perf_counter() < t_end:
+            time.sleep(0.01)   # first sample = NVML initialised
+        self.first = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -100,7 +110,7 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for line in self.lines[self.first:]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -188,6 +198,8 @@ def gpu_run(args, conf):
     cfg = P.RunConfig(rank=R, algorithm=conf["algo"], max_iters=args.warmup + args.steps + 1, tol=0.0,
                       seed=INIT_SEED, cuda_graph=False if args.eager else None)
     eng = _Engine(x_local, layout.local_dims, dims, cfg, coll, layout if world > 1 else None, timing=False)
+    clocks = ClockSampler(dev)
+    clocks.start()
     eng.initialise()
     eng.iterate(args.warmup)
 
@@ -196,12 +208,11 @@ def gpu_run(args, conf):
             dist.barrier()
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(dev)
     eng.ctx.kernel_events = []
     launches0 = _lib.load().nncp_launch_count()
     replays0 = eng.graph_replays
     barrier()
-    clocks.start()
+    clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
