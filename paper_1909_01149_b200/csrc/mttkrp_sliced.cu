@@ -231,6 +231,7 @@ struct BSpec {
   const int* rowexp;  // nullable
   int64_t K, Kp, Kc;  // Kp: K rounded up to whole 128-deep k blocks
   int R, RP;
+  int segg;           // segment-reuse path: outer indices per block (<= SEG_G)
 };
 
 constexpr int EXP_NONE = int(0x80808080);   // memset(0x80) sentinel: column chunk has no nonzero
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(256) bslice_digits_kernel(BSpec s, const int* 
 // other factors each: every factor row is read once per block instead of once
 // per KRP row.  Each lane's 16 consecutive rows give 16 consecutive bytes of
 // each digit plane (one 16-byte store per plane, no transpose).
-constexpr int SEG_G = 16;   // outer indices per block
+constexpr int SEG_G = 16;   // outer indices per block (at most; fewer when that leaves SMs idle)
 
 template <int NF, int H>
 struct SegCursor {
@@ -465,7 +466,7 @@ template <int NF, int H>
 __global__ void __launch_bounds__(256) bseg_exp_kernel(BSpec s, int* __restrict__ bexp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nseg = s.dim[0] / BK, outer = s.K / s.dim[0];
-  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * SEG_G;
+  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * s.segg;
   const int64_t i0 = seg * BK + warp * 16;        // first factor-0 row of the warp
   double h0[16][H];
 #pragma unroll
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(256) bseg_exp_kernel(BSpec s, int* __restrict_
 #pragma unroll
   for (int h = 0; h < H; ++h) mx[h] = 0.0;
   int64_t chunk = -1;
-  const int64_t oend = min(outer, o0 + SEG_G);
+  const int64_t oend = min(outer, o0 + s.segg);
   SegLoads<NF, H> nxt;
   nxt.load(s, cur, i0 + s.dim[0] * o0, lane, o0 < oend);
   for (int64_t o = o0; o < oend; ++o) {
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __
   extern __shared__ __align__(16) uint8_t stage[];   // L * RP rows x SEG_PITCH bytes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nseg = s.dim[0] / BK, outer = s.K / s.dim[0];
-  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * SEG_G;
+  const int64_t seg = blockIdx.x, o0 = int64_t(blockIdx.y) * s.segg;
   const int64_t i0 = seg * BK + warp * 16;
   const int nrow = L * s.RP;
   double h0[16][H];
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __
       h0[i][h] = lane + 32 * h < s.R ? __ldg(s.ptr[0] + (i0 + i) * s.R + lane + 32 * h) : 0.0;
   SegCursor<NF, H> cur;
   cur.init(s, o0, lane);
-  const int64_t oend = min(outer, o0 + SEG_G);
+  const int64_t oend = min(outer, o0 + s.segg);
   SegLoads<NF, H> nxt;
   nxt.load(s, cur, i0 + s.dim[0] * o0, lane, o0 < oend);
   for (int64_t o = o0; o < oend; ++o) {
@@ -592,9 +593,12 @@ int launch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaS
 }
 
 template <int L, int NF, int H>
-int launch_bseg(const BSpec& b, int* bexp, int8_t* bs, cudaStream_t st) {
-  const int64_t outer = b.K / b.dim[0];
-  const dim3 grid{unsigned(b.dim[0] / BK), unsigned((outer + SEG_G - 1) / SEG_G), 1u};
+int launch_bseg(const BSpec& b0, int* bexp, int8_t* bs, cudaStream_t st) {
+  BSpec b = b0;
+  const int64_t outer = b.K / b.dim[0], nseg = b.dim[0] / BK;
+  // >= ~4 blocks per SM (512^3: 4 segments x 512 outer indices -> 3 per block, 684 blocks)
+  b.segg = int(std::max<int64_t>(1, std::min<int64_t>(SEG_G, nseg * outer / (4 * int64_t(num_sms())))));
+  const dim3 grid{unsigned(nseg), unsigned((outer + b.segg - 1) / b.segg), 1u};
   bseg_exp_kernel<NF, H><<<grid, 256, 0, st>>>(b, bexp);
   NNCP_LAUNCH_CHECK();
   static bool attr = false;

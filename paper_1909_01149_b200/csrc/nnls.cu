@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
-  load_hadamard(S, grams, order, mode, R);
+  // HALS walks column r of S across the lanes: keep S^T (St[r][c] = S[c][r])
+  load_hadamard<ALGO == NNCP_ALGO_HALS>(S, grams, order, mode, R);
   __syncthreads();
   if (ALGO == NNCP_ALGO_HALS && blockIdx.x == 0) {
     for (int r = threadIdx.x; r < R; r += blockDim.x)
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int cc = lane + 32 * q;
-          if (cc < R) p = fma(h[q], S[cc * R + r], p);
+          if (cc < R) p = fma(h[q], S[r * R + cc], p);   // S^T[r][cc] = S[cc][r]
         }
         const double dot = warp_sum(p);
         if ((r & 31) == lane) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(kBppWarps * 32)
   double* colbuf = red + kBppWarps * 64;              // RP + 1
   double* lu = colbuf + RP + 1;                       // kBppWarps * RP * LP
   int* pidx_all = reinterpret_cast<int*>(lu + size_t(kBppWarps) * RP * LP);   // kBppWarps * 64
-  load_hadamard(S, grams, order, mode, R);
+  load_hadamard<true>(S, grams, order, mode, R);   // S^T: the gathers below walk columns across lanes
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* A = lu + size_t(warp) * RP * LP;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kBppWarps * 32)
       __syncwarp();
       for (int a = lane; a < p; a += 32) {
         const int ra = pidx[a];
-        for (int b = 0; b < p; ++b) A[a * LP + b] = S[ra * R + pidx[b]];
+        for (int b = 0; b < p; ++b) A[a * LP + b] = S[pidx[b] * R + ra];   // S^T[pb][ra] = S[ra][pb]
         A[a * LP + p] = fr[ra];
       }
       __syncwarp();
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kBppWarps * 32)
             for (int b = 0; b < p; ++b) {
               const int rb = __ffsll(nn) - 1;
               nn &= nn - 1;
-              s = fma(S[r * R + rb], A[b * LP + p], s);
+              s = fma(S[rb * R + r], A[b * LP + p], s);   // S^T[rb][r] = S[r][rb]
             }
             ys[q] = s - fs[q];
           }
@@ -325,11 +326,24 @@ __global__ void __launch_bounds__(256)
   if (gram == nullptr) return;  // row scaling only
   const int RR = R * R;
   double* mypart = part + size_t(blockIdx.x) * RR;
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-    const int a = e / R, b = e - (e / R) * R;
-    double s = 0.0;
-    for (int il = 0; il < nr; ++il) s = fma(tile[il * RP + a], tile[il * RP + b], s);
-    mypart[e] = s;
+  // four entries per thread in flight (four independent FMA chains over the rows)
+  for (int e0 = threadIdx.x; e0 < RR; e0 += 4 * blockDim.x) {
+    int ia[4], ib[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int e = min(e0 + o * int(blockDim.x), RR - 1);
+      ia[o] = e / R;
+      ib[o] = e - (e / R) * R;
+    }
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int il = 0; il < nr; ++il) {
+      const double* tr = tile + il * RP;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) s[o] = fma(tr[ia[o]], tr[ib[o]], s[o]);
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+      if (e0 + o * int(blockDim.x) < RR) mypart[e0 + o * blockDim.x] = s[o];
   }
   if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, RR, gram);
 }

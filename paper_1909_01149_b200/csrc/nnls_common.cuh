@@ -7,6 +7,10 @@ namespace nncp {
 
 // --------------------------------------------------------------- helpers --
 // S[a][b] = prod_{m != mode} 0.5 (G_m[a][b] + G_m[b][a]); order==0: S = grams.
+// TRANSPOSED: store S^T instead (identical for order > 0, where S is symmetric bit
+// for bit), so kernels that walk a column of S across lanes read a row instead:
+// lane-consecutive addresses, no 32-way shared-memory bank conflict at R = 32.
+template <bool TRANSPOSED = false>
 static __device__ void load_hadamard(double* S, const double* __restrict__ grams, int order, int mode, int R) {
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int a = e / R, b = e - (e / R) * R;
@@ -21,7 +25,7 @@ static __device__ void load_hadamard(double* S, const double* __restrict__ grams
         v *= 0.5 * (g[a * R + b] + g[b * R + a]);
       }
     }
-    S[e] = v;
+    S[TRANSPOSED ? b * R + a : e] = v;
   }
 }
 
@@ -41,9 +45,10 @@ static __device__ double block_sum(double v, double* red) {
 
 // Final fixed-order reduction of per-CTA partials [nblk][n] -> out[n], run by the
 // last CTA.  Latency-bound if done naively (one thread walking nblk partials), so
-// each output is split into `segs` strided segments with four independent
-// accumulators, then the segments are summed in order: deterministic for a given
-// launch configuration.  Needs blockDim.x doubles of shared scratch.
+// the loads are issued in independent batches: with n <= blockDim.x each output
+// is split into `segs` strided segments with eight accumulators, then the segments
+// are summed in order; otherwise a thread owns four outputs and issues 4 x 4 loads
+// per step.  Deterministic for a given launch configuration.
 static __device__ void finish_partials(const double* part, int nblk, int n, double* out) {
   __shared__ double seg_sum[1024];
   const int T = blockDim.x;
@@ -53,16 +58,19 @@ static __device__ void finish_partials(const double* part, int nblk, int n, doub
     const int t = threadIdx.x;
     if (t < n * segs) {
       const int e = t % n, sg = t / n;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      double a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = 0.0;
       int b = sg;
-      for (; b + 3 * segs < nblk; b += 4 * segs) {
-        a0 += part[size_t(b) * n + e];
-        a1 += part[size_t(b + segs) * n + e];
-        a2 += part[size_t(b + 2 * segs) * n + e];
-        a3 += part[size_t(b + 3 * segs) * n + e];
+      for (; b + 7 * segs < nblk; b += 8 * segs) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = part[size_t(b + q * segs) * n + e];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] += v[q];
       }
-      for (; b < nblk; b += segs) a0 += part[size_t(b) * n + e];
-      seg_sum[sg * n + e] = (a0 + a1) + (a2 + a3);
+      for (; b < nblk; b += segs) a[0] += part[size_t(b) * n + e];
+      seg_sum[sg * n + e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     __syncthreads();
     for (int e = threadIdx.x; e < n; e += T) {
@@ -71,17 +79,29 @@ static __device__ void finish_partials(const double* part, int nblk, int n, doub
       out[e] = s;
     }
   } else {
-    for (int e = threadIdx.x; e < n; e += T) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int b = 0;
-      for (; b + 3 < nblk; b += 4) {
-        a0 += part[size_t(b) * n + e];
-        a1 += part[size_t(b + 1) * n + e];
-        a2 += part[size_t(b + 2) * n + e];
-        a3 += part[size_t(b + 3) * n + e];
+    for (int e0 = threadIdx.x; e0 < n; e0 += 4 * T) {
+      double a[4][4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[o][q] = 0.0;
+      for (int b = 0; b < nblk; b += 4) {
+        double v[4][4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = e0 + o * T;
+            v[o][q] = (e < n && b + q < nblk) ? part[size_t(b + q) * n + e] : 0.0;
+          }
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[o][q] += v[o][q];
       }
-      for (; b < nblk; ++b) a0 += part[size_t(b) * n + e];
-      out[e] = (a0 + a1) + (a2 + a3);
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        if (e0 + o * T < n) out[e0 + o * T] = (a[o][0] + a[o][1]) + (a[o][2] + a[o][3]);
     }
   }
 }

@@ -273,3 +273,21 @@ def test_sliced_balanced_split_run(P):
             assert np.max(np.abs(a - b)) <= FACTOR_TOL
     with pytest.raises(ValueError, match="dimtree_split"):
         P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=r, dimtree_split="middle"))
+
+
+def test_sliced_balanced_split_grid_run(P):
+    """Thread-simulated 2x2x1 grid on a skewed shape: every worker's block takes the balanced split
+    (local 48x24x8: S = 1); the grid run matches the oracle's sequential run."""
+    rng = np.random.default_rng(37)
+    dims, r = (96, 48, 8), 6
+    hs = [rng.random((d, r)) for d in dims]
+    x = O.reconstruct(hs, np.ones(r))
+    errors, factors, _, _, _ = O.run_sequential(x, dims, r, "hals", 6, 0.0, 0)
+    cfg = P.RunConfig(rank=r, algorithm="hals", max_iters=6, tol=0.0, grid=(2, 2, 1), mttkrp_kernel="sliced")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        par = P.nncp_parallel(P.DenseTensor(dims, x), cfg)
+    assert par.split_mode == 1
+    assert np.max(np.abs(np.array(par.errors) - np.array(errors))) <= TRACE_TOL
+    for a, b in zip(par.model.factors, factors):
+        assert np.max(np.abs(a - b)) <= FACTOR_TOL
