@@ -54,17 +54,29 @@ def build(verbose: bool = False) -> str:
     return OUT
 
 
-def build_stats() -> str:
-    """Instrumented variant (barrier wait counters in the sliced GEMM) for tools/sliced_stats.py."""
-    out = os.path.join(HERE, "libnncp_b200_stats.so")
+def build_variant(name: str, defines) -> str:
+    """A tools-only variant of the library (loaded through NNCP_LIB_PATH), e.g. with extra -D flags."""
+    out = os.path.join(HERE, f"libnncp_b200_{name}.so")
     os.makedirs(BUILD, exist_ok=True)
+    extra = tuple(f"-D{d}" for d in defines)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = [o for o, _ in ex.map(lambda s: _compile(s, ("-DNNCP_SLICED_STATS",), "_stats"), SOURCES)]
+        objs = [o for o, _ in ex.map(lambda s: _compile(s, extra, "_" + name), SOURCES)]
     res = subprocess.run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-lcudart"], capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     return out
 
 
+def build_stats() -> str:
+    """Instrumented variant (barrier wait counters in the sliced GEMM) for tools/sliced_stats.py."""
+    return build_variant("stats", ["NNCP_SLICED_STATS"])
+
+
 if __name__ == "__main__":
-    print(build_stats() if "--stats" in sys.argv else build(verbose="-v" in sys.argv))
+    if "--stats" in sys.argv:
+        print(build_stats())
+    elif "--variant" in sys.argv:   # --variant NAME DEFINE [DEFINE ...]
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(verbose="-v" in sys.argv))
