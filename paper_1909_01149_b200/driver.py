@@ -54,8 +54,9 @@ class RunConfig:
     ``cuda_graph`` (device-only): after the first sweep, the whole sweep of
     launches (including the per-category timing events) is replayed as one
     CUDA graph.  ``None`` (default) enables it whenever the sweep is
-    capturable (one execution context, MU/HALS/BPP/UCP); ``False`` forces
-    eager launches.
+    capturable (MU/HALS/BPP/UCP, one execution context or one process per GPU
+    with in-place NCCL collectives, which are captured with the kernels);
+    ``False`` forces eager launches.
     """
 
     rank: int
@@ -576,7 +577,8 @@ class _Engine:
         """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
         cfg = self.cfg
         errors = self.report.errors
-        capturable = not self.coll.parallel and cfg.algorithm in FUSED_ALGORITHMS
+        capturable = ((not self.coll.parallel or getattr(self.coll, "capturable", False))
+                      and cfg.algorithm in FUSED_ALGORITHMS)
         use_graph = capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
@@ -587,6 +589,8 @@ class _Engine:
                 self._capture()
             if self.graph is not None:
                 self.graph.replay()
+                if self.graph_replays:
+                    self._replay_counters()
                 self.graph_replays += 1
                 if cfg.use_dimtree:
                     self.ctx.partial_calls += 2
@@ -614,6 +618,7 @@ class _Engine:
         """Record one sweep as a CUDA graph (all buffers already allocated by sweep 1)."""
         calls = self.ctx.partial_calls
         launches0 = self.lib.nncp_launch_count()
+        comm0 = self.coll.counters.snapshot()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -628,12 +633,28 @@ class _Engine:
             warnings.warn(f"CUDA graph capture failed, continuing without graphs: {exc}")
             torch.cuda.current_stream().wait_stream(side)
             self.ctx.partial_calls = calls
+            self._restore_counters(comm0)
             self.graph_failed = True
             return
         torch.cuda.current_stream().wait_stream(side)
         self.ctx.partial_calls = calls
         self.graph_kernels = int(self.lib.nncp_launch_count() - launches0)
+        # the collectives recorded once while capturing belong to the first replay;
+        # later replays add the same calls and words (grid.py:60-93 tallies per call)
+        comm1 = self.coll.counters.snapshot()
+        self.graph_comm = {k: {name: v - comm0[k].get(name, 0) for name, v in comm1[k].items()} for k in comm1}
         self.graph = g
+
+    def _replay_counters(self):
+        c = self.coll.counters
+        for name, calls in self.graph_comm["calls"].items():
+            c.calls[name] = c.calls.get(name, 0) + calls
+            c.words_in[name] = c.words_in.get(name, 0) + self.graph_comm["words_in"].get(name, 0)
+            c.words_out[name] = c.words_out.get(name, 0) + self.graph_comm["words_out"].get(name, 0)
+
+    def _restore_counters(self, snap):
+        c = self.coll.counters
+        c.calls, c.words_in, c.words_out = (dict(snap["calls"]), dict(snap["words_in"]), dict(snap["words_out"]))
 
     def model_host(self):
         return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()

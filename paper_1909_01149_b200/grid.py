@@ -214,6 +214,10 @@ class DistCollectives:
         # gloo moves host memory only: device tensors are staged through the host
         # (CPU tests and the single-GPU multi-process test); NCCL works in place.
         self.stage = dist.get_backend() == "gloo"
+        # NCCL collectives run in place on the current stream, so a whole sweep
+        # (kernels + collectives) can be captured as one CUDA graph; the
+        # host-staged gloo path cannot.
+        self.capturable = not self.stage
         grid = layout.grid
         if dist_groups is None:
             dist_groups = make_slice_process_groups(grid)

@@ -84,3 +84,69 @@ def test_spmd_processes_match_reference_grid_run(golden, case):
         # merged counters: the reference's per-worker collective calls summed over workers
         if str(g[f"{name}_algo"]) != "hals":
             assert calls == list(g[f"{tag}_calls"])
+
+
+def _nccl_graph_worker(port, out_q):
+    """World-size-1 NCCL job: nncp_parallel on the trivial grid goes through
+    DistCollectives (in-place NCCL all-reduces on the current stream), so the
+    sweep graph captures the collectives together with the kernels."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_1909_01149_b200 as P
+        from tests.conftest import load_golden
+
+        g = load_golden("runs.npz")
+        res = {}
+        for name in ("hals_odd", "bpp3", "mu4"):
+            dims = tuple(int(d) for d in g[f"{name}_dims"])
+            r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
+            algo = str(g[f"{name}_algo"])
+            x = P.DenseTensor(dims, g[f"{name}_x"])
+            out = {}
+            for mode in (None, False):
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    warnings.filterwarnings("error", message="CUDA graph capture failed")
+                    cfg = P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed,
+                                      grid=(1,) * len(dims), cuda_graph=mode)
+                    rep = P.nncp_parallel(x, cfg)
+                out[mode] = (rep.errors, [np.asarray(f) for f in rep.model.factors], rep.counters.snapshot())
+            seq = P.nncp_sequential(x, P.RunConfig(rank=r, algorithm=algo, max_iters=iters, tol=0.0, seed=iseed))
+            res[name] = (out, seq.errors, [np.asarray(f) for f in seq.model.factors])
+        out_q.put(res)
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+
+        out_q.put(repr(exc) + traceback.format_exc())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_sweep_graph_capture_matches_eager_and_sequential():
+    """The NCCL grid path captured as a CUDA graph: bitwise the eager NCCL run and
+    the sequential run, with the collective counters of the eager run."""
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_graph_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=900)
+    p.join(timeout=120)
+    assert not isinstance(res, str), res
+    for name, (out, seq_err, seq_f) in res.items():
+        (eg, fg, cg), (ee, fe, ce) = out[None], out[False]
+        assert eg == ee == seq_err, name
+        for a, b, c in zip(fg, fe, seq_f):
+            assert np.array_equal(a, b) and np.array_equal(a, c), name
+        assert cg == ce, (name, cg, ce)
+        assert cg["calls"]["AllReduce"] > 0
