@@ -130,6 +130,8 @@ int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_ro
 
 /* Status reset on the stream (see status words above). */
 int nncp_status_reset(int* status, void* stream);
+/* The same for `count` consecutive status blocks (one per mode) in one launch. */
+int nncp_status_reset_n(int* status, int count, void* stream);
 
 /* Fused NNLS factor update (driver.py:396-418 first half + updaters.py):
  *   S = prod_{m != mode} sym(G_m)          (tensor_ops.py:146-155), or when order == 0

@@ -33,7 +33,7 @@ int normalize_gram(const double*, const double*, int64_t, int, double*, double*,
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
 int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
-int status_reset(int*, cudaStream_t);
+int status_reset(int*, int, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
 int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
         cudaStream_t);
@@ -211,7 +211,12 @@ int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_ro
   return temp_to_rows(temp, rows, rank, out_rows, S(stream));
 }
 
-int nncp_status_reset(int* status, void* stream) { return status_reset(status, S(stream)); }
+int nncp_status_reset(int* status, void* stream) { return status_reset(status, 1, S(stream)); }
+
+int nncp_status_reset_n(int* status, int count, void* stream) {
+  if (count < 1) return fail(NNCP_ERR_VALUE, "status block count must be positive");
+  return status_reset(status, count, S(stream));
+}
 
 int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                 const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,

@@ -645,13 +645,24 @@ __global__ void ttv_partials_reduce_kernel(const double* __restrict__ tpart, int
     int64_t c_lo = (ib * nout * ctas) / items;
     while (c_lo > 0 && (c_lo * items) / ctas > ib * nout) --c_lo;
     while (c_lo < ctas - 1 && ((c_lo + 1) * items) / ctas <= ib * nout) ++c_lo;
+    // contributing CTAs: c_lo .. while the CTA's first item is inside block ib (monotone
+    // in c); four partials loaded ahead of the in-order additions (same sum order)
+    const int64_t end_item = (ib + 1) * nout;
     double s = 0.0;
-    for (int64_t c = c_lo; c < ctas; ++c) {
-      const int64_t b = c * items / ctas, en = (c + 1) * items / ctas;
-      if (b >= (ib + 1) * nout) break;
-      if (en <= b) continue;
-      const int64_t ib0 = b / nout;
-      s += tpart[((c * slots + (ib - ib0)) * 128 + row) * RP + r];
+    for (int64_t c = c_lo; c < ctas; c += 4) {
+      double v[4];
+      bool ok[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t cc = c + q;
+        const int64_t b = cc * items / ctas, en = (cc + 1) * items / ctas;
+        ok[q] = cc < ctas && b < end_item && en > b;
+        v[q] = ok[q] ? tpart[((cc * slots + (ib - b / nout)) * 128 + row) * RP + r] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ok[q]) s += v[q];
+      if (c + 4 >= ctas || (c + 4) * items / ctas >= end_item) break;
     }
     out1[e] = s;
   }

@@ -437,11 +437,14 @@ __global__ void __launch_bounds__(512)
   }
 }
 
-__global__ void status_reset_kernel(int* status) {
-  status[0] = 0;
-  status[1] = 0;
-  status[2] = INT_MAX;
-  status[3] = 0;
+__global__ void status_reset_kernel(int* status, int count) {
+  for (int b = threadIdx.x; b < count; b += blockDim.x) {
+    int* s = status + b * NNCP_STATUS_WORDS;
+    s[0] = 0;
+    s[1] = 0;
+    s[2] = INT_MAX;
+    s[3] = 0;
+  }
 }
 
 // ------------------------------------------------------------- host side ---
@@ -557,8 +560,8 @@ int norm_squared(const double* x, int64_t n, double* out, double* out_min, void*
   return NNCP_OK;
 }
 
-int status_reset(int* status, cudaStream_t st) {
-  status_reset_kernel<<<1, 1, 0, st>>>(status);
+int status_reset(int* status, int count, cudaStream_t st) {
+  status_reset_kernel<<<1, 32, 0, st>>>(status, count);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

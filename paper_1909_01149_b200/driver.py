@@ -433,8 +433,8 @@ class _Engine:
         cfg = self.cfg
         if cfg.use_dimtree:
             self.ctx.begin_iteration()
+        _lib.check(lib.nncp_status_reset_n(_lib.ptr(self.status), N, st))
         for n in range(N):
-            _lib.check(lib.nncp_status_reset(_lib.ptr(self.status[n]), st))
             mb = self.mbar[: self.dims[n]]
             if cfg.use_dimtree:
                 self.ctx.mttkrp(self.x, self.shared, n, out=mb)
@@ -622,12 +622,19 @@ class _Engine:
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
+        # capture_begin/end directly: torch.cuda.graph's context manager also
+        # empties the allocator caches (device and pinned host) first, which made the
+        # capturing iteration ~19 ms slower at 2048^3 (measured)
         try:
+            torch.cuda.synchronize()
             with torch.cuda.stream(side):
-                with torch.cuda.graph(g, stream=side):
+                g.capture_begin()
+                try:
                     self.timer.begin_capture()
                     self._sweep()
                     self.timer.end_capture()
+                finally:
+                    g.capture_end()
         except Exception as exc:  # noqa: BLE001  (stay on the eager path, still correct)
             self.timer.capturing = False
             warnings.warn(f"CUDA graph capture failed, continuing without graphs: {exc}")

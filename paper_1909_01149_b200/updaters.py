@@ -161,6 +161,16 @@ def _host(t: torch.Tensor):
     return t.detach().cpu().numpy()
 
 
+def _runner_rows(capacity: int, m: torch.Tensor, *others: torch.Tensor) -> int:
+    """Rows of this call: the MTTKRP block's (a grid rank owns a different row count per
+    mode; the runner's buffers are sized for the largest).  Launching with the buffer
+    capacity would read past the smaller operands."""
+    rows = int(m.shape[0])
+    if rows > capacity or any(int(t.shape[0]) < rows for t in others):
+        raise ValueError(f"inner-solver operands disagree on rows: {rows} (capacity {capacity})")
+    return rows
+
+
 class AdmmRunner:
     """Inner loop of admm_update on device buffers (updaters.py:173-220)."""
 
@@ -179,13 +189,14 @@ class AdmmRunner:
         status = self.status if status is None else status
         if rho is not None and rho <= 0.0:
             raise ValueError("rho must be positive")
+        rows = _runner_rows(self.rows, m, current, u)
         x = current
         steps = 0
         for k in range(max_steps):
             out = self.buf[k % 2]
             _lib.check(lib.nncp_admm_step(_lib.ptr(spack.grams), spack.order, spack.mode, self.rank,
                                           float(rho) if rho is not None else -1.0, _lib.ptr(m), _lib.ptr(x),
-                                          _lib.ptr(u), _lib.ptr(out), self.rows, _lib.ptr(self.sums),
+                                          _lib.ptr(u), _lib.ptr(out), rows, _lib.ptr(self.sums),
                                           _lib.ptr(status), self.ws.ptr, self.ws.nbytes, st))
             x = out
             steps += 1
@@ -252,6 +263,7 @@ class NesterovRunner:
             max_iters: int = NESTEROV_INNER_CAP, tol: float = 1e-8):
         lib = _lib.load()
         st = _lib.stream_handle()
+        rows = _runner_rows(self.rows, m, current, xstar)
         _lib.check(lib.nncp_nes_hyper(_lib.ptr(spack.grams), spack.order, spack.mode, self.rank,
                                       NESTEROV_PROX_FLOOR, _lib.ptr(self.hyper), st))
         x = y = current
@@ -260,7 +272,7 @@ class NesterovRunner:
             xo, yo = self.x[k % 2], self.y[k % 2]
             _lib.check(lib.nncp_nes_step(_lib.ptr(spack.grams), spack.order, spack.mode, self.rank,
                                          _lib.ptr(self.hyper), _lib.ptr(m), _lib.ptr(y), _lib.ptr(x),
-                                         _lib.ptr(xstar), _lib.ptr(xo), _lib.ptr(yo), self.rows,
+                                         _lib.ptr(xstar), _lib.ptr(xo), _lib.ptr(yo), rows,
                                          _lib.ptr(self.maxes), self.ws.ptr, self.ws.nbytes, st))
             steps += 1
             red = hook(self.maxes, "max")

@@ -132,3 +132,39 @@ def test_uneven_dims_and_blocks_all_algorithms(P, algo):
     assert np.allclose(seq.errors, par.errors, rtol=0, atol=tol)
     for a, b in zip(seq.model.factors, par.model.factors):
         assert np.allclose(a, b, rtol=0, atol=max(tol, 1e-10) * 100)
+
+
+@pytest.mark.parametrize("algo", ["admm", "nes"])
+def test_inner_runner_uses_call_rows_not_capacity(P, algo):
+    """A grid rank's runner is sized for its largest owned block; a call with fewer rows
+    must touch only those rows (regression: the launch used the capacity, read past the
+    smaller operands and let stale memory into the stopping test)."""
+    import torch
+    from paper_1909_01149_b200.tensor_ops import Workspace
+    from paper_1909_01149_b200.updaters import AdmmRunner, NesterovRunner, _SPack, local_reduce
+
+    rng = np.random.default_rng(3)
+    r, rows, cap = 4, 3, 11
+    a = rng.random((9, r))
+    s = torch.tensor(a.T @ a, dtype=torch.float64, device="cuda")
+    dev = dict(dtype=torch.float64, device="cuda")
+    m_np = rng.random((rows, r))
+    res = []
+    for capacity in (rows, cap):
+        # operands are views into NaN-filled buffers with room behind them
+        back = [torch.full((cap, r), float("nan"), **dev) for _ in range(3)]
+        m, cur, aux = (b[:rows] for b in back)
+        m.copy_(torch.tensor(m_np, **dev))
+        cur.copy_(m * 0.5)
+        if algo == "admm":
+            aux.zero_()
+        else:
+            aux.copy_(cur)
+        runner = (AdmmRunner if algo == "admm" else NesterovRunner)(capacity, r, torch.device("cuda"),
+                                                                   Workspace(1 << 20))
+        for buf in (runner.buf if algo == "admm" else runner.x + runner.y):
+            buf.fill_(float("nan"))
+        x, steps = runner.run(_SPack.explicit(s), m, cur, aux, local_reduce)
+        res.append((x[:rows].cpu().numpy(), steps))
+    assert np.isfinite(res[0][0]).all()
+    assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
