@@ -43,6 +43,9 @@ CONFIGS = {
     "c5mu": dict(dims=(2048, 2048, 2048), rank=32, algo="mu", eta=0.01, kind="uniform"),
     # the per-GPU block of c5 on the 2x2x2 grid: 1-GPU proxy for the 8-GPU strong-scaling step
     "c5blk8": dict(dims=(1024, 1024, 1024), rank=32, algo="hals", eta=0.01, kind="uniform"),
+    # per-GPU blocks of c4 (2x2x2) and c3 (2x2x2x1): 1-GPU proxies for their 8-GPU steps
+    "c4blk8": dict(dims=(2048, 1024, 128), rank=20, algo="hals", eta=0.05, kind="walk"),
+    "c3blk8": dict(dims=(128, 128, 128, 256), rank=32, algo="bpp", eta=0.01, kind="uniform"),
 }
 GRIDS = {3: {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)},
          4: {1: (1, 1, 1, 1), 2: (2, 1, 1, 1), 4: (2, 2, 1, 1), 8: (2, 2, 2, 1)}}

@@ -471,7 +471,7 @@ size_t row_update_part_elems(int64_t rows, int rank) {
   const int64_t blocks_gram = (rows + kGramRows - 1) / kGramRows;
   size_t e = std::max<int64_t>(blocks_rows, blocks_bpp) * (rank + 6);  // + ADMM/NES step partials
   e = std::max<size_t>(e, size_t(std::max<int64_t>(blocks_gram, 1)) * rank * rank);
-  e = std::max<size_t>(e, size_t(num_sms()) * 8);
+  e = std::max<size_t>(e, size_t(num_sms()) * 8 * 2);   // norm_squared(_min): <= 8 blocks/SM, sum + min each
   return e;
 }
 

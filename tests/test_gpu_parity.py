@@ -336,7 +336,10 @@ def test_grid_runs_bitwise_reproducible(P, golden):
 
 @pytest.mark.parametrize("dims,r,algo,iters", [((128, 128, 128), 16, "hals", 8), ((32, 32, 32, 32), 32, "bpp", 4),
                                                ((256, 128, 16), 20, "hals", 6), ((96, 80, 64), 64, "mu", 5),
-                                               ((160, 144, 120), 24, "bpp", 4)])
+                                               ((160, 144, 120), 24, "bpp", 4),
+                                               # many elements, short modes, low rank: the initial norm
+                                               # pass's partials size the workspace (found by fuzzing)
+                                               ((37, 25, 3, 33, 21), 8, "mu", 2)])
 def test_runs_vs_oracle_tma_sizes(P, dims, r, algo, iters):
     """Full sequential runs on the TMA/split-K paths (BASELINE config shapes scaled down) vs the oracle."""
     rng = np.random.default_rng(sum(dims) * r)
