@@ -70,7 +70,8 @@ for case in range(cases):
                   f"{'' if ok else '  <-- FAIL'}", flush=True)
             fails += 0 if ok else 1
             continue
-        dt = float(np.max(np.abs(np.array(rep.errors) - np.array(errors))))
+        # traces compared relative to max(1, eps): a tensor scaled by 2^-60 starts at eps ~ 1e15
+        dt = float(np.max(np.abs(np.array(rep.errors) - np.array(errors)) / np.maximum(1.0, np.abs(errors))))
         df = max(float(np.max(np.abs(a - b))) for a, b in zip(rep.model.factors, factors))
         bad = dt > tol or df > 1e-6
         grid_msg = ""
@@ -83,12 +84,13 @@ for case in range(cases):
                 if len(par.errors) != len(errors):
                     print(f"{tag}: grid {grid} exact fit, traces stop at {len(par.errors)} / {len(errors)}", flush=True)
                     continue
-                dg = float(np.max(np.abs(np.array(par.errors) - np.array(errors))))
+                dg = float(np.max(np.abs(np.array(par.errors) - np.array(errors)) / np.maximum(1.0, np.abs(errors))))
                 dgf = max(float(np.max(np.abs(a - b))) for a, b in zip(par.model.factors, factors))
                 grid_msg = f" grid {grid}: trace {dg:.1e} factors {dgf:.1e}"
                 bad = bad or dg > tol or dgf > 1e-6
         if bad:
             fails += 1
+            print(f"  device {np.array(rep.errors)}\n  oracle {np.array(errors)}", flush=True)
         print(f"{tag}: trace {dt:.1e} factors {df:.1e}{grid_msg}{'  <-- FAIL' if bad else ''}", flush=True)
     except Exception:  # noqa: BLE001
         fails += 1
