@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -27,6 +28,21 @@ int fail(int code, const std::string& msg);
     if (_e != cudaSuccess)                                                           \
       return ::nncp::fail(NNCP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
+
+// Opt a kernel in to more than 48 KB of dynamic shared memory, once per device
+// (the attribute lives in the device context; flags are atomic because the
+// thread-simulated grid launches from several host threads).
+template <auto Kernel>
+inline int set_max_smem_once(int bytes) {
+  static std::atomic<unsigned long long> done{0ull};
+  int dev = 0;
+  NNCP_CUDA_TRY(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  NNCP_CUDA_TRY(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.fetch_or(bit, std::memory_order_release);
+  return 0;
+}
 
 void count_launch();
 #define NNCP_LAUNCH_CHECK()            \

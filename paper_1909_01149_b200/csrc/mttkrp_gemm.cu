@@ -574,12 +574,7 @@ template <int RP, int NFM>
 int launch_left_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
                    int R, cudaStream_t st) {
   using T = LeftTile<RP>;
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_left_tma<RP, NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(T::SMEM)));
-    attr = true;
-  }
+  if (int rc = set_max_smem_once<mttkrp_left_tma<RP, NFM>>(int(T::SMEM))) return rc;
   const int64_t items = p.tiles * p.splits;
   const unsigned ctas = unsigned(std::min<int64_t>(items, num_sms()));
   mttkrp_left_tma<RP, NFM><<<ctas, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, p.tiles, items, dst,
@@ -592,12 +587,7 @@ template <int RP, int NFM>
 int launch_right_nf(const CUtensorMap& map, const KrpSpec& krp, const PartialPlan& p, double* dst, int64_t stride,
                     int R, cudaStream_t st) {
   using T = RightTile<RP>;
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(mttkrp_right_tma<RP, NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(T::SMEM)));
-    attr = true;
-  }
+  if (int rc = set_max_smem_once<mttkrp_right_tma<RP, NFM>>(int(T::SMEM))) return rc;
   dim3 grid(unsigned(p.tiles), unsigned(p.splits));
   mttkrp_right_tma<RP, NFM><<<grid, T::THREADS, T::SMEM, st>>>(map, krp, p.M, p.J, p.per_split, dst, stride, R);
   NNCP_LAUNCH_CHECK();

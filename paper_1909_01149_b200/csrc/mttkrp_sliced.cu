@@ -579,12 +579,7 @@ __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __
 
 template <int L, int NF, int H>
 int launch_bslice(const BSpec& b, int* bexp, int8_t* bs, unsigned kblocks, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(bslice_digits_kernel<L, NF, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(L * kMaxRank * 33 * 4)));
-    attr = true;
-  }
+  if (int rc = set_max_smem_once<bslice_digits_kernel<L, NF, H>>(int(L * kMaxRank * 33 * 4))) return rc;
   bslice_exp_kernel<NF, H><<<kblocks, 256, 0, st>>>(b, bexp);
   NNCP_LAUNCH_CHECK();
   bslice_digits_kernel<L, NF, H><<<kblocks, 256, size_t(L) * b.RP * 33 * 4, st>>>(b, bexp, bs);
@@ -601,12 +596,7 @@ int launch_bseg(const BSpec& b0, int* bexp, int8_t* bs, cudaStream_t st) {
   const dim3 grid{unsigned(nseg), unsigned((outer + b.segg - 1) / b.segg), 1u};
   bseg_exp_kernel<NF, H><<<grid, 256, 0, st>>>(b, bexp);
   NNCP_LAUNCH_CHECK();
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(bseg_digits_kernel<L, NF, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(L * kMaxRank * SEG_PITCH)));
-    attr = true;
-  }
+  if (int rc = set_max_smem_once<bseg_digits_kernel<L, NF, H>>(int(L * kMaxRank * SEG_PITCH))) return rc;
   bseg_digits_kernel<L, NF, H><<<grid, 256, size_t(L) * b.RP * SEG_PITCH, st>>>(b, bexp, bs);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
@@ -1185,12 +1175,7 @@ template <int SIDE, int RP, int L>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& ga,
                 cudaStream_t st) {
   using C = GemmCfg<RP, L, SIDE>;
-  static bool attr = false;
-  if (!attr) {
-    NNCP_CUDA_TRY(cudaFuncSetAttribute(sliced_gemm_kernel<SIDE, RP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(C::SMEM)));
-    attr = true;
-  }
+  if (int rc = set_max_smem_once<sliced_gemm_kernel<SIDE, RP, L>>(int(C::SMEM))) return rc;
   const unsigned ctas = unsigned(std::min<int64_t>(ga.items, num_sms()));
   sliced_gemm_kernel<SIDE, RP, L><<<ctas, THREADS, C::SMEM, st>>>(ma, mb, mo, ga);
   NNCP_LAUNCH_CHECK();

@@ -191,15 +191,27 @@ __global__ void __launch_bounds__(kBppWarps * 32)
           const bool cand = bi != INT_MAX;
           const unsigned long long bits = cand ? (unsigned long long)__double_as_longlong(bv) : 0ull;
           const uint32_t mh = __reduce_max_sync(0xffffffffu, uint32_t(bits >> 32));
-          const uint32_t ml = __reduce_max_sync(0xffffffffu, (cand && uint32_t(bits >> 32) == mh) ? uint32_t(bits) : 0u);
-          const bool win = cand && uint32_t(bits >> 32) == mh && uint32_t(bits) == ml;
-          bi = int(__reduce_min_sync(0xffffffffu, win ? uint32_t(bi) : 0xffffffffu));
-          bv = __hiloint2double(int(mh), int(ml));
+          const unsigned tie = __ballot_sync(0xffffffffu, cand && uint32_t(bits >> 32) == mh);
+          if (__popc(tie) == 1) {   // one lane holds the high-word maximum: its (value, row) wins
+            const int src = __ffs(tie) - 1;
+            bi = __shfl_sync(0xffffffffu, bi, src);
+            bv = __shfl_sync(0xffffffffu, bv, src);
+          } else {
+            const uint32_t ml =
+                __reduce_max_sync(0xffffffffu, (cand && uint32_t(bits >> 32) == mh) ? uint32_t(bits) : 0u);
+            const bool win = cand && uint32_t(bits >> 32) == mh && uint32_t(bits) == ml;
+            bi = int(__reduce_min_sync(0xffffffffu, win ? uint32_t(bi) : 0xffffffffu));
+            bv = __hiloint2double(int(mh), int(ml));
+          }
         }
         if (!(bv > 0.0)) {
           singular = true;
           break;
         }
+        // the pivot (row bi before the swap); its reciprocal overlaps the swap
+        const double piv = A[bi * LP + cidx];
+        __syncwarp();
+        const double inv = 1.0 / piv;
         if (bi != cidx) {
           for (int b = lane; b <= p; b += 32) {
             const double t0 = A[cidx * LP + b];
@@ -208,7 +220,6 @@ __global__ void __launch_bounds__(kBppWarps * 32)
           }
         }
         __syncwarp();
-        const double inv = 1.0 / A[cidx * LP + cidx];
         for (int a = cidx + 1 + lane; a < p; a += 32) {
           const double l = A[a * LP + cidx] * inv;
           A[a * LP + cidx] = l;
@@ -235,12 +246,36 @@ __global__ void __launch_bounds__(kBppWarps * 32)
         fail_kind = 2;
         break;
       }
-      // back substitution, solution overwrites column p
-      for (int a = p - 1; a >= 0; --a) {
-        double s = 0.0;
-        for (int b = a + 1 + lane; b < p; b += 32) s = fma(A[a * LP + b], A[b * LP + p], s);
-        s = warp_sum(s);
-        if (lane == 0) A[a * LP + p] = (A[a * LP + p] - s) / A[a * LP + a];
+      // back substitution in column (axpy) order, as dtrsm does it: the right-hand
+      // side lives in registers (lane k holds rows k, k + 32); per step one division
+      // on the owning lane, one broadcast, one FMA per remaining row -- no warp
+      // reduction on the sequential chain.  The solution overwrites column p.
+      {
+        double bq[NH];
+#pragma unroll
+        for (int q = 0; q < NH; ++q) {
+          const int k = lane + 32 * q;
+          bq[q] = k < p ? A[k * LP + p] : 0.0;
+        }
+        for (int a = p - 1; a >= 0; --a) {
+          const int src = a & 31, qa = a >> 5;
+          double mine = 0.0;
+#pragma unroll
+          for (int q = 0; q < NH; ++q)
+            if (q == qa) mine = bq[q];
+          const double xa = __shfl_sync(0xffffffffu, mine / A[a * LP + a], src);
+#pragma unroll
+          for (int q = 0; q < NH; ++q) {
+            const int k = lane + 32 * q;
+            if (k == a) bq[q] = xa;
+            else if (k < a) bq[q] = fma(-A[k * LP + a], xa, bq[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NH; ++q) {
+          const int k = lane + 32 * q;
+          if (k < p) A[k * LP + p] = bq[q];
+        }
         __syncwarp();
       }
       // scatter x, compute y on the active set
@@ -503,11 +538,7 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
       const size_t smem = sizeof(double) * (size_t(RP) * RP + kBppWarps * 64 + RP + 1 +
                                             size_t(kBppWarps) * RP * (RP + 1)) +
                           sizeof(int) * kBppWarps * 64;
-      static bool attr = false;
-      if (!attr) {
-        NNCP_CUDA_TRY(cudaFuncSetAttribute(bpp_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = true;
-      }
+      if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;
       bpp_kernel<RP><<<blocks, kBppWarps * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
                                                            beta, status, w.tickets + T_UPDATE);
     });
