@@ -41,15 +41,19 @@ for case in range(cases):
     if rng.random() < 0.1:
         x = x * 2.0 ** float(rng.integers(-60, 60))
     seed = int(rng.integers(0, 100))
-    tag = f"case {case}: dims {dims} R={rank} {algo} {engine}"
+    extra = dict(mttkrp_levels=int(rng.choice([6, 6, 7])), dimtree_split=str(rng.choice(["auto", "reference"])),
+                 strict_split=bool(rng.random() < 0.2), use_dimtree=bool(rng.random() < 0.85),
+                 cuda_graph=[None, False][int(rng.random() < 0.3)])
+    tag = f"case {case}: dims {dims} R={rank} {algo} {engine} {extra}"
     try:
         try:
-            ref = O.run_sequential(x, dims, rank, algo, iters, 0.0, seed)
+            ref = O.run_sequential(x, dims, rank, algo, iters, 0.0, seed, use_dimtree=extra["use_dimtree"],
+                                   strict_split=extra["strict_split"])
         except Exception as exc:  # noqa: BLE001  (the reference fails too: device must fail alike)
             ref = exc
         try:
             rep = P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=rank, algorithm=algo, max_iters=iters,
-                                                                        tol=0.0, seed=seed, mttkrp_kernel=engine))
+                                                                        tol=0.0, seed=seed, mttkrp_kernel=engine, **extra))
         except Exception as exc:  # noqa: BLE001
             if isinstance(ref, Exception):
                 print(f"{tag}: both fail ({type(ref).__name__} / {type(exc).__name__})", flush=True)
@@ -80,7 +84,7 @@ for case in range(cases):
             if np.prod(grid) > 1:
                 par = P.nncp_parallel(P.DenseTensor(dims, x), P.RunConfig(rank=rank, algorithm=algo, max_iters=iters,
                                                                            tol=0.0, seed=seed, grid=grid,
-                                                                           mttkrp_kernel=engine))
+                                                                           mttkrp_kernel=engine, **extra))
                 if len(par.errors) != len(errors):
                     print(f"{tag}: grid {grid} exact fit, traces stop at {len(par.errors)} / {len(errors)}", flush=True)
                     continue
