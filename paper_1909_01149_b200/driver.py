@@ -253,7 +253,7 @@ SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
 _HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 5e-5
 
 
-def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6) -> bool:
+def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6, extra_bytes: int = 0) -> bool:
     """Resolve RunConfig.mttkrp_kernel for one execution context."""
     if kind == "fp64":
         return False
@@ -267,7 +267,33 @@ def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6) ->
     if t_sliced >= t_fp64:
         return False
     free, _ = torch.cuda.mem_get_info(dev)
-    return SlicedTensor.nbytes(dims, split, levels) + SLICED_HBM_MARGIN <= free
+    free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)   # torch's cached blocks
+    return SlicedTensor.nbytes(dims, split, levels) + SLICED_HBM_MARGIN + extra_bytes <= free
+
+
+def _engine_plan(dims, cfg: RunConfig, dev, extra_bytes: int = 0):
+    """Dimension-tree plan and partial-MTTKRP engine of one execution context:
+    (plan, sliced?).  ``extra_bytes``: device memory still to be allocated first."""
+    plan = DimTreePlan.create(dims, int(cfg.rank), cfg.strict_split)
+    if not _use_sliced(cfg.mttkrp_kernel, dims, plan.split, int(cfg.rank), dev, cfg.mttkrp_levels, extra_bytes):
+        return plan, False
+    if cfg.dimtree_split == "auto":
+        s_bal = choose_balanced_split(dims)
+        if 2 * _split_rows(dims, s_bal) <= _split_rows(dims, plan.split):
+            plan = DimTreePlan(dims, int(cfg.rank), s_bal)
+    return plan, True
+
+
+def _reserve_sliced(dims, cfg: RunConfig):
+    """Before a host tensor is copied in: allocate and release the sliced tensor's
+    buffer through torch's caching allocator while the device is idle.  cudaMalloc
+    waits for pending device work, so allocating the ~50 GB buffer behind the
+    asynchronous H2D would serialise on the copy; the cached block is reused by
+    SlicedTensor with no driver call."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    plan, sliced = _engine_plan(dims, cfg, dev, extra_bytes=8 * math.prod(dims))
+    if sliced:
+        torch.empty(SlicedTensor.nbytes(dims, plan.split, cfg.mttkrp_levels), dtype=torch.uint8, device=dev)
 
 
 def _split_rows(dims, s: int) -> int:
@@ -300,13 +326,9 @@ class _Engine:
             self.slice_rows = list(layout.slice_rows)
             self.owned_parts = list(layout.owned_parts)
         self.n_owned = [s.stop - s.start for s in self.owned_rows]
-        self.plan = DimTreePlan.create(self.dims, self.R, cfg.strict_split)
+        self.plan, use_sliced = _engine_plan(self.dims, cfg, dev)
         self.sliced = None
-        if _use_sliced(cfg.mttkrp_kernel, self.dims, self.plan.split, self.R, dev, cfg.mttkrp_levels):
-            if cfg.dimtree_split == "auto":
-                s_bal = choose_balanced_split(self.dims)
-                if 2 * _split_rows(self.dims, s_bal) <= _split_rows(self.dims, self.plan.split):
-                    self.plan = DimTreePlan(self.dims, self.R, s_bal)
+        if use_sliced:
             self.sliced = SlicedTensor(x_local, self.dims, self.plan.split, cfg.mttkrp_levels)
         ws_bytes = self.plan.workspace_bytes()
         if self.sliced is not None:
@@ -693,6 +715,8 @@ def nncp_sequential(x: DenseTensor, cfg: RunConfig) -> RunReport:
     cfg.validate(x.order)
     if cfg.grid is not None and int(np.prod(cfg.grid)) != 1:
         raise ValueError("sequential driver got a nontrivial grid; use nncp_parallel")
+    if not x.on_device:
+        _reserve_sliced(x.dims, cfg)
     xd = x.to_device()
     # the negative-entry warning comes from the engine's first pass over the tensor
     eng, rep = run_local(xd.data, x.dims, x.dims, cfg, warn_negative=True)

@@ -119,8 +119,21 @@ class DenseTensor:
         return isinstance(self.data, torch.Tensor) and self.data.is_cuda
 
     def to_device(self) -> "DenseTensor":
-        """Same tensor with its buffer resident in HBM."""
-        return self if self.on_device else DenseTensor(self.dims, as_device(self.data))
+        """Same tensor with its buffer resident in HBM.
+
+        From page-locked host memory the copy is queued asynchronously on the
+        current stream, so the engine's allocations (the sliced tensor, tens of GB
+        at the BASELINE sizes) and host-side setup overlap the transfer; every
+        consumer is ordered behind it on the stream.
+        """
+        if self.on_device:
+            return self
+        d = self.data
+        if isinstance(d, torch.Tensor) and d.is_pinned() and d.dtype == torch.float64 and d.is_contiguous():
+            out = torch.empty(d.numel(), dtype=torch.float64, device=device())
+            out.copy_(d.reshape(-1), non_blocking=True)
+            return DenseTensor(self.dims, out)
+        return DenseTensor(self.dims, as_device(d))
 
     def host_data(self) -> np.ndarray:
         if isinstance(self.data, torch.Tensor):
