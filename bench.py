@@ -358,7 +358,11 @@ def main():
                     "bound": "hbm", "algorithmic": f"{alg:.4g} B per launch ({L} digit planes {planes:.4g} B + "
                                                    f"factor digits + fp64 output)",
                     "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
-                    "peak_source": hbm_src + " (of measured)"}
+                    "peak_source": hbm_src + " (of measured)",
+                    "peak_note": ("the peak is a device-to-device copy (half reads, half writes); this kernel's "
+                                  "traffic is ~98% reads, which stream faster (read-only probe 6.87 TB/s, "
+                                  "profiles/r01_peaks_probe.log; ncu shows 7.0-7.2 TB/s for the GEMMs), hence "
+                                  "frac > 1")}
     else:
         t_sliced_roof = None
         bound = "tensor" if 2.0 * R / FP64_PEAK_TFLOPS / 1e12 >= 8.0 / hbm_gbs / 1e9 else "hbm"
