@@ -375,15 +375,23 @@ __global__ void __launch_bounds__(256) bslice_digits_kernel(BSpec s, const int* 
     if (r >= s.RP) continue;
     const int e = r < s.R ? bexp[chunk * s.RP + r] : EXP_NONE;
     const int k = 8 * L - 2 - (e == EXP_NONE ? 0 : e);   // digits of (v 2^rowexp) / 2^e
+    auto digits = [&](auto scale) {   // range of 2^k tested once per column (see bseg_digits_kernel)
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      int lo[4], hi[4];
+      for (int g = 0; g < 4; ++g) {
+        int lo[4], hi[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) scale_halves<L>(v[4 * g + i][h] * sc[4 * g + i], k, lo[i], hi[i]);
-      uint32_t w[L];
-      pack4<L>(lo, hi, w);
+        for (int i = 0; i < 4; ++i) slice_halves<L>(scale(v[4 * g + i][h] * sc[4 * g + i]), lo[i], hi[i]);
+        uint32_t w[L];
+        pack4<L>(lo, hi, w);
 #pragma unroll
-      for (int t = 0; t < L; ++t) tile[(t * s.RP + r) * 33 + warp * 4 + g] = w[t];
+        for (int t = 0; t < L; ++t) tile[(t * s.RP + r) * 33 + warp * 4 + g] = w[t];
+      }
+    };
+    if (k >= -1022 && k <= 1023) {
+      const double p2 = __longlong_as_double((long long)(k + 1023) << 52);
+      digits([p2](double x) { return x * p2; });
+    } else {
+      digits([k](double x) { return scalbn(x, k); });
     }
   }
   __syncthreads();
@@ -554,15 +562,26 @@ __global__ void __launch_bounds__(256) bseg_digits_kernel(BSpec s, const int* __
       const int e = r < s.R ? __ldg(bexp + c * s.RP + r) : EXP_NONE;
       const int kx = 8 * L - 2 - (e == EXP_NONE ? 0 : e);
       uint32_t w[4][L];
+      // the column's scaling 2^kx is uniform over the 16 rows: test its range once
+      // and branch (scale_halves' per-element select kept the scalbn path in the
+      // issue stream, predicated off); the arithmetic is scale_halves' in both arms
+      auto digits = [&](auto scale) {
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        int lo[4], hi[4];
+        for (int q4 = 0; q4 < 4; ++q4) {
+          int lo[4], hi[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double sc = __longlong_as_double((long long)(now.rexp(4 * q4 + i) + 1023) << 52);
-          scale_halves<L>(h0[4 * q4 + i][h] * now.g[h] * sc, kx, lo[i], hi[i]);
+          for (int i = 0; i < 4; ++i) {
+            const double sc = __longlong_as_double((long long)(now.rexp(4 * q4 + i) + 1023) << 52);
+            slice_halves<L>(scale(h0[4 * q4 + i][h] * now.g[h] * sc), lo[i], hi[i]);
+          }
+          pack4<L>(lo, hi, w[q4]);
         }
-        pack4<L>(lo, hi, w[q4]);
+      };
+      if (kx >= -1022 && kx <= 1023) {
+        const double p2 = __longlong_as_double((long long)(kx + 1023) << 52);
+        digits([p2](double v) { return v * p2; });
+      } else {
+        digits([kx](double v) { return scalbn(v, kx); });
       }
 #pragma unroll
       for (int t = 0; t < L; ++t)
