@@ -189,35 +189,48 @@ __global__ void __launch_bounds__(256) slice_planes_kernel(const double* __restr
   const int64_t mb = m0 / BM;
   const int64_t j0 = int64_t(blockIdx.y) * jper;
   const int64_t j1 = min(Jp, j0 + jper);
-  for (int64_t j = j0; j < j1; ++j) {
-    double v[16];
-    const double* src = x + M * j + m0;
-    if (j >= J) {
+  // the 16 rows' scalings 2^(8L-2-ex) are fixed for the whole column range: test their
+  // range once (scale_halves' per-element select kept its scalbn path in the issue
+  // stream); both arms compute exactly what scale_halves does
+  auto sweep = [&](auto scale) {
+    for (int64_t j = j0; j < j1; ++j) {
+      double v[16];
+      const double* src = x + M * j + m0;
+      if (j >= J) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.0;
-    } else if (VEC && m0 + 16 <= M) {
+        for (int i = 0; i < 16; ++i) v[i] = 0.0;
+      } else if (VEC && m0 + 16 <= M) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double2 t = __ldcs(reinterpret_cast<const double2*>(src) + i);
-        v[2 * i] = t.x;
-        v[2 * i + 1] = t.y;
+        for (int i = 0; i < 8; ++i) {
+          const double2 t = __ldcs(reinterpret_cast<const double2*>(src) + i);
+          v[2 * i] = t.x;
+          v[2 * i + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
       }
-    } else {
+      uint32_t w[4][L];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
+      for (int g4 = 0; g4 < 4; ++g4) {
+        int lo[4], hi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) slice_halves<L>(scale(v[4 * g4 + i], 4 * g4 + i), lo[i], hi[i]);
+        pack4<L>(lo, hi, w[g4]);
+      }
+      int8_t* blk = planes + ((mb * njb + j / BK) * L) * int64_t(TILE) + (j % BK) * BM + (m0 % BM);
+#pragma unroll
+      for (int s = 0; s < L; ++s)
+        *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[0][s], w[1][s], w[2][s], w[3][s]);
     }
-    uint32_t w[4][L];
+  };
+  bool fast = true;
 #pragma unroll
-    for (int g4 = 0; g4 < 4; ++g4) {
-      int lo[4], hi[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) scale_halves<L>(v[4 * g4 + i], 8 * L - 2 - ex[4 * g4 + i], lo[i], hi[i]);
-      pack4<L>(lo, hi, w[g4]);
-    }
-    int8_t* blk = planes + ((mb * njb + j / BK) * L) * int64_t(TILE) + (j % BK) * BM + (m0 % BM);
-#pragma unroll
-    for (int s = 0; s < L; ++s)
-      *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[0][s], w[1][s], w[2][s], w[3][s]);
+  for (int i = 0; i < 16; ++i) fast = fast && (8 * L - 2 - ex[i] >= -1022) && (8 * L - 2 - ex[i] <= 1023);
+  if (fast) {
+    sweep([&ex](double v, int i) { return v * __longlong_as_double((long long)(8 * L - 2 - ex[i] + 1023) << 52); });
+  } else {
+    sweep([&ex](double v, int i) { return scalbn(v, 8 * L - 2 - ex[i]); });
   }
 }
 
