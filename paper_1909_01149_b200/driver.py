@@ -612,7 +612,7 @@ class _Engine:
             if self.graph is not None:
                 self.graph.replay()
                 if self.graph_replays:
-                    self._replay_counters()
+                    self.coll.counters.add(self.graph_comm)
                 self.graph_replays += 1
                 if cfg.use_dimtree:
                     self.ctx.partial_calls += 2
@@ -662,7 +662,7 @@ class _Engine:
             warnings.warn(f"CUDA graph capture failed, continuing without graphs: {exc}")
             torch.cuda.current_stream().wait_stream(side)
             self.ctx.partial_calls = calls
-            self._restore_counters(comm0)
+            self.coll.counters.restore(comm0)
             self.graph_failed = True
             return
         torch.cuda.current_stream().wait_stream(side)
@@ -670,20 +670,8 @@ class _Engine:
         self.graph_kernels = int(self.lib.nncp_launch_count() - launches0)
         # the collectives recorded once while capturing belong to the first replay;
         # later replays add the same calls and words (grid.py:60-93 tallies per call)
-        comm1 = self.coll.counters.snapshot()
-        self.graph_comm = {k: {name: v - comm0[k].get(name, 0) for name, v in comm1[k].items()} for k in comm1}
+        self.graph_comm = self.coll.counters.since(comm0)
         self.graph = g
-
-    def _replay_counters(self):
-        c = self.coll.counters
-        for name, calls in self.graph_comm["calls"].items():
-            c.calls[name] = c.calls.get(name, 0) + calls
-            c.words_in[name] = c.words_in.get(name, 0) + self.graph_comm["words_in"].get(name, 0)
-            c.words_out[name] = c.words_out.get(name, 0) + self.graph_comm["words_out"].get(name, 0)
-
-    def _restore_counters(self, snap):
-        c = self.coll.counters
-        c.calls, c.words_in, c.words_out = (dict(snap["calls"]), dict(snap["words_in"]), dict(snap["words_out"]))
 
     def model_host(self):
         return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()

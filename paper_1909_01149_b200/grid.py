@@ -89,6 +89,23 @@ class CommCounters:
     def snapshot(self) -> dict:
         return {"calls": dict(self.calls), "words_in": dict(self.words_in), "words_out": dict(self.words_out)}
 
+    def since(self, snap: dict) -> dict:
+        """Calls and words recorded after ``snap`` (one captured sweep's collectives)."""
+        now = self.snapshot()
+        return {k: {name: v - snap[k].get(name, 0) for name, v in now[k].items()} for k in now}
+
+    def add(self, delta: dict):
+        """Re-add a ``since`` delta (a CUDA-graph replay of the captured collectives)."""
+        for name, calls in delta["calls"].items():
+            self.calls[name] = self.calls.get(name, 0) + calls
+            self.words_in[name] = self.words_in.get(name, 0) + delta["words_in"].get(name, 0)
+            self.words_out[name] = self.words_out.get(name, 0) + delta["words_out"].get(name, 0)
+
+    def restore(self, snap: dict):
+        """Back to ``snap`` (a capture that failed recorded calls that never ran)."""
+        self.calls, self.words_in, self.words_out = (dict(snap["calls"]), dict(snap["words_in"]),
+                                                     dict(snap["words_out"]))
+
     def total_words(self) -> int:
         return sum(self.words_in.values()) + sum(self.words_out.values())
 

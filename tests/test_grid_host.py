@@ -64,3 +64,26 @@ def test_counters_merge():
     m = a.merged_with(b)
     assert m.calls == {"AllReduce": 2, "AllGather": 1}
     assert m.total_words() == 3 + 3 + 2 + 2 + 4 + 8
+
+
+def test_counters_graph_replay_delta():
+    """A sweep captured once as a CUDA graph records its collectives once; every later
+    replay re-adds exactly that delta, and a failed capture restores the snapshot."""
+    c = CommCounters()
+    c.record("AllReduce", 4, 4)
+    snap = c.snapshot()
+    sweep = [("ReduceScatter", 32, 16), ("AllReduce", 2, 2), ("AllGather", 16, 32), ("AllReduce", 4, 4)]
+    for name, a, b in sweep:          # the capture records the sweep once
+        c.record(name, a, b)
+    delta = c.since(snap)
+    assert delta["calls"] == {"AllReduce": 2, "ReduceScatter": 1, "AllGather": 1}
+    for _ in range(3):                # three more replays
+        c.add(delta)
+    ref = CommCounters()
+    ref.record("AllReduce", 4, 4)
+    for _ in range(4):
+        for name, a, b in sweep:
+            ref.record(name, a, b)
+    assert c.snapshot() == ref.snapshot()
+    c.restore(snap)
+    assert c.snapshot() == snap
