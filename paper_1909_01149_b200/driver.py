@@ -366,6 +366,9 @@ class _Engine:
                 self.runner = NesterovRunner(rows_max, R, dev, self.ws)
                 self.nes_prev = [None] * N
         self.graph = None
+        # capture stream created up front: torch's first Stream() builds its stream pool
+        # (~14 ms, measured), which here overlaps an asynchronous tensor upload
+        self.capture_stream = torch.cuda.Stream() if cfg.cuda_graph is not False else None
         self.graph_failed = False
         self.graph_kernels = 0      # library kernels captured in the sweep graph
         self.graph_replays = 0
@@ -642,7 +645,7 @@ class _Engine:
         launches0 = self.lib.nncp_launch_count()
         comm0 = self.coll.counters.snapshot()
         g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
+        side = self.capture_stream or torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         # capture_begin/end directly: torch.cuda.graph's context manager also empties
         # the allocator caches (device and pinned host), which this capture does not
