@@ -198,6 +198,25 @@ def test_cuda_graph_matches_eager(P, golden):
         assert all(sum(row.values()) > 0 for row in graph.rows[1:])
 
 
+@pytest.mark.parametrize("engine", ["fp64", "sliced"])
+def test_pinned_host_input_matches_numpy_and_device_input(P, golden, engine):
+    """nncp_sequential on a page-locked host tensor (asynchronous upload, sliced buffer
+    reserved before the copy) gives bitwise the run on a numpy array and on a CUDA tensor."""
+    import torch
+
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, "hals_r16")
+    cfg.mttkrp_kernel = engine
+    host = np.ascontiguousarray(x.host_data())
+    pinned = torch.from_numpy(host.copy()).pin_memory()
+    runs = [P.nncp_sequential(P.DenseTensor(x.dims, d), cfg)
+            for d in (host, pinned, torch.from_numpy(host.copy()).cuda())]
+    for rep in runs[1:]:
+        assert rep.errors == runs[0].errors
+        for a, b in zip(rep.model.factors, runs[0].model.factors):
+            assert np.array_equal(a, b)
+
+
 def test_run_to_run_determinism(P, golden):
     g = golden("runs.npz")
     _, _, _, _, x, cfg = _run_case(P, g, "bpp_r32")
