@@ -1061,10 +1061,17 @@ __global__ void __launch_bounds__(THREADS, 1) sliced_gemm_kernel(const __grid_co
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            double s = double(int(v[L - 1][i]));
-#pragma unroll
-            for (int l = L - 2; l >= 0; --l) s = fma(s, 0.00390625, double(int(v[l][i])));
-            acc[rg * 8 + i] += times_pow2(s, eb[rg * 8 + i]);
+            // sum_l acc_l 2^(-8l): levels combined three at a time in exact int64
+            // (|acc_l| < 2^31, so each group < 2^48 converts exactly), then one fp64
+            // rounding per pair of groups -- two conversions instead of six
+            const long long g1 = (long long)int(v[0][i]) * 65536ll + (long long)int(v[1][i]) * 256ll +
+                                 (long long)int(v[2][i]);
+            const long long g2 = (long long)int(v[3][i]) * 65536ll + (long long)int(v[4][i]) * 256ll +
+                                 (long long)int(v[5][i]);
+            double lowp = double(g2);
+            if constexpr (L == 7) lowp = lowp + double(int(v[6][i])) * 0x1p-8;   // level 6: 2^-8 below level 5
+            const double s = double(g1) + lowp * 0x1p-24;   // = 2^16 sum_l acc_l 2^(-8l)
+            acc[rg * 8 + i] += times_pow2(s, eb[rg * 8 + i] - 16);
           }
         }
         tc_fence_before();

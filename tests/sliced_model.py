@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE ONLY.  It restates, operation by operation, what
 paper_1909_01149_b200/csrc/mttkrp_sliced.cu computes -- the row exponents and
 balanced base-256 digits of X_(1:S), the per-(chunk, column) exponents and
 digits of the Khatri-Rao side, the exact integer level sums of the tensor-core
-MMAs, the fp64 epilogue (Horner over the levels, power-of-two scaling,
+MMAs, the fp64 epilogue (levels grouped in exact int64, power-of-two scaling,
 chunk-ordered accumulation) and the split-K group plan and fixed-order group
 reduction -- so that
 
@@ -153,9 +153,15 @@ def sliced_partial(x, dims, split, side, factors, rank, levels=6, sms=148):
                 for s in range(lvl + 1):
                     t += a_d[s][:, sl] @ bd[lvl - s][sl]
                 lev.append(t)
-            v = lev[levels - 1].astype(np.float64)
-            for lvl in range(levels - 2, -1, -1):
-                v = v * 0.00390625 + lev[lvl].astype(np.float64)
+            # the kernel's epilogue: levels combined three at a time in exact int64,
+            # one fp64 rounding per pair of groups (L = 7: the seventh level joins
+            # the low group first)
+            g1 = lev[0] * 65536 + lev[1] * 256 + lev[2]
+            g2 = lev[3] * 65536 + lev[4] * 256 + lev[5]
+            low = g2.astype(np.float64)
+            if levels == 7:
+                low = low + lev[6].astype(np.float64) * 2.0 ** -8
+            v = (g1.astype(np.float64) + low * 2.0 ** -24) * 2.0 ** -16
             e = row_e[:, None] + np.where(none[c], 0, eb[c])[None, :] - 12
             acc = acc + np.ldexp(v, e)
         parts.append(acc)
