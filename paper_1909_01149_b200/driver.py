@@ -380,8 +380,7 @@ class _Engine:
 
     def _gather(self, n):
         if self.coll.parallel:
-            out = self.coll.all_gather(n, self.owned[n], self.owned_parts[n])
-            self.shared[n].copy_(out)
+            self.coll.all_gather(n, self.owned[n], self.owned_parts[n], out=self.shared[n])
 
     # -- initialisation (driver.py:338-373) -----------------------------------
     def initialise(self):

@@ -209,7 +209,10 @@ class IdentityCollectives:
     def reduce_scatter(self, mode, t, parts=None):
         return t
 
-    def all_gather(self, mode, t, parts=None):
+    def all_gather(self, mode, t, parts=None, out=None):
+        if out is not None and out is not t:
+            out.copy_(t)
+            return out
         return t
 
 
@@ -280,12 +283,18 @@ class DistCollectives:
         self.counters.record("ReduceScatter", t.numel(), out.numel())
         return out
 
-    def all_gather(self, mode, t, parts):
+    def all_gather(self, mode, t, parts, out=None):
+        """Slice-group All-Gather of the owned rows; ``out`` (optional, rows x R) receives
+        the gathered block directly when the group's blocks are equal (no padding,
+        no concatenation copy)."""
         group = self.layout.groups[mode]
         r = int(t.shape[1])
         width = parts.max_length
         if group.size == 1:
-            out = t
+            res = t
+        elif not (self.stage and t.is_cuda) and all(x == width for x in parts.lengths):
+            res = out if out is not None else torch.empty((group.size * width, r), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(res.reshape(-1), t.contiguous().reshape(-1), group=self.slice_pg[mode])
         else:
             src = torch.zeros((width, r), dtype=t.dtype, device=t.device)
             src[: t.shape[0]] = t
@@ -296,9 +305,12 @@ class DistCollectives:
             else:
                 full = torch.empty((group.size, width, r), dtype=t.dtype, device=t.device)
                 self.dist.all_gather_into_tensor(full.reshape(-1), src.reshape(-1), group=self.slice_pg[mode])
-            out = torch.cat([full[k, : parts.lengths[k]] for k in range(group.size)], dim=0)
-        self.counters.record("AllGather", t.numel(), out.numel())
-        return out
+            res = torch.cat([full[k, : parts.lengths[k]] for k in range(group.size)], dim=0)
+        if out is not None and res is not out:
+            out.copy_(res)
+            res = out
+        self.counters.record("AllGather", t.numel(), res.numel())
+        return res
 
 
 def make_slice_process_groups(grid: Grid):
@@ -405,17 +417,20 @@ class ThreadCollectives:
         self.counters.record("ReduceScatter", t.numel(), out.numel())
         return out
 
-    def all_gather(self, mode, t, parts):
+    def all_gather(self, mode, t, parts, out=None):
         group = self.layout.groups[mode]
         me = group.index[self.layout.rank]
         rv = self.tgrid.slice_rv[mode][self.layout.coord[mode]]
         self._sync()
 
         def combine(slots):
-            out = torch.cat(slots, dim=0)
+            res = torch.cat(slots, dim=0)
             self._sync()
-            return out
+            return res
 
-        out = rv.exchange(me, t, combine)
-        self.counters.record("AllGather", t.numel(), out.numel())
-        return out
+        res = rv.exchange(me, t, combine)
+        self.counters.record("AllGather", t.numel(), res.numel())
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res

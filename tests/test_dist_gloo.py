@@ -52,6 +52,11 @@ def _worker(rank, world, port, grid, dims, r, out_q):
                                        lay.owned_parts[n])
             res[f"ag{n}"] = float(np.max(np.abs(gathered.numpy() - hs[n][lay.slice_rows[n]]))) \
                 if gathered.numel() else 0.0
+            # into a caller buffer (the engine gathers straight into its slice rows)
+            dst = torch.full((lay.local_dims[n], r), np.nan, dtype=torch.float64)
+            back = coll.all_gather(n, torch.from_numpy(np.ascontiguousarray(hs[n][lay.owned_rows[n]])),
+                                   lay.owned_parts[n], out=dst)
+            res[f"ago{n}"] = (back is dst, bool(np.array_equal(dst.numpy(), hs[n][lay.slice_rows[n]])))
         t = torch.full((r * r + r,), float(rank + 1), dtype=torch.float64)
         coll.all_reduce(t)
         res["ar"] = float(t[0])
@@ -86,13 +91,14 @@ def test_gloo_collectives_reproduce_global_mttkrp(grid, dims, r):
         for n in range(len(dims)):
             assert res[f"rs{n}"] <= 1e-12, (k, n)
             assert res[f"ag{n}"] == 0.0, (k, n)
+            assert res[f"ago{n}"] == (True, True), (k, n)
         assert res["ar"] == sum(range(1, world + 1))
         calls, win, wout = res["counters"]
-        assert calls["ReduceScatter"] == len(dims) and calls["AllGather"] == len(dims)
+        assert calls["ReduceScatter"] == len(dims) and calls["AllGather"] == 2 * len(dims)
         assert calls["AllReduce"] == 1 and win["AllReduce"] == r * r + r
         # reference cost model: Reduce-Scatter input = I_n/P_n rows x R (test_acceptance.py:243-252)
         from paper_1909_01149_b200.grid import Grid, RankLayout
 
         lay = RankLayout(Grid(grid), k, dims)
         assert win["ReduceScatter"] == sum(d * r for d in lay.local_dims)
-        assert wout["AllGather"] == sum(d * r for d in lay.local_dims)
+        assert wout["AllGather"] == 2 * sum(d * r for d in lay.local_dims)
