@@ -38,13 +38,15 @@ for case in range(cases):
     x = x + 0.05 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))
     if signed:
         x = x - np.mean(x)
+    scale = 0
     if rng.random() < 0.1:
-        x = x * 2.0 ** float(rng.integers(-60, 60))
+        scale = int(rng.integers(-60, 60))
+        x = x * 2.0 ** scale
     seed = int(rng.integers(0, 100))
     extra = dict(mttkrp_levels=int(rng.choice([6, 6, 7])), dimtree_split=str(rng.choice(["auto", "reference"])),
                  strict_split=bool(rng.random() < 0.2), use_dimtree=bool(rng.random() < 0.85),
                  cuda_graph=[None, False][int(rng.random() < 0.3)])
-    tag = f"case {case}: dims {dims} R={rank} {algo} {engine} {extra}"
+    tag = f"case {case}: dims {dims} R={rank} {algo} {engine} {extra}" + (f" x*2^{scale}" if scale else "")
     try:
         try:
             ref = O.run_sequential(x, dims, rank, algo, iters, 0.0, seed, use_dimtree=extra["use_dimtree"],
