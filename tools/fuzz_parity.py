@@ -2,7 +2,7 @@
 engines against the oracle (sequential) and against the sequential device run
 (thread-simulated grids).  Bug hunting beyond the fixed test cases.
 
-    python tools/fuzz_parity.py [cases] [seed]
+    python tools/fuzz_parity.py [cases] [seed] [log2 max elements] [--large]
 """
 import sys
 import traceback
@@ -14,22 +14,33 @@ sys.path.insert(0, ".")
 import paper_1909_01149_b200 as P  # noqa: E402
 from oracle import nncp_oracle as O  # noqa: E402
 
-cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
-rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+cases = int(args[0]) if len(args) > 0 else 60
+rng = np.random.default_rng(int(args[1]) if len(args) > 1 else 7)
 warnings.simplefilter("ignore")
+LARGE = "--large" in sys.argv
 fails = 0
 for case in range(cases):
-    order = int(rng.integers(2, 6))
-    budget = 1 << int(rng.integers(10, int(sys.argv[3]) if len(sys.argv) > 3 else 19))
-    dims = []
-    for _ in range(order):
-        dims.append(int(rng.integers(1, 48)))
-    while np.prod(dims) > budget:
-        k = int(np.argmax(dims))
-        dims[k] = max(1, dims[k] // 2)
-    dims = tuple(dims)
+    if LARGE:   # 2^22..2^24 elements: the sizes where "auto" picks the sliced engine
+        order = int(rng.integers(3, 5))
+        target = 2.0 ** float(rng.uniform(22, 24))
+        w = rng.dirichlet(np.ones(order))
+        dims = tuple(max(2, int(round(target ** wi))) for wi in w)
+    else:
+        order = int(rng.integers(2, 6))
+        budget = 1 << int(rng.integers(10, int(args[2]) if len(args) > 2 else 19))
+        dims = []
+        for _ in range(order):
+            dims.append(int(rng.integers(1, 48)))
+        while np.prod(dims) > budget:
+            k = int(np.argmax(dims))
+            dims[k] = max(1, dims[k] // 2)
+        dims = tuple(dims)
     rank = int(rng.choice([1, 2, 3, 7, 8, 16, 17, 31, 32, 33, 40, 64]))
     algo = str(rng.choice(["mu", "hals", "bpp", "ucp", "admm", "nes"]))
+    if LARGE:
+        rank = int(rng.choice([8, 16, 20, 32, 33, 48, 64]))
+        algo = str(rng.choice(["mu", "hals", "bpp"]))
     engine = str(rng.choice(["fp64", "sliced", "auto"]))
     signed = bool(rng.random() < 0.15) and algo in ("ucp",)
     iters = 4
