@@ -11,9 +11,11 @@ needed between steps).  For N > 1 (torchrun) the tensor is split over the
 reference's N-d grid (2x1x1 / 2x2x1 / 2x2x2), one block per GPU, NCCL
 collectives; the total work is fixed (strong scaling).
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-numpy port in oracle/, the reference being pure Python + numpy) on this host's
-cores over a bounded slab of the same workload.
+``--impl reference`` times the UNMODIFIED reference ``nncp_sequential`` (pure
+Python + numpy/OpenBLAS, installed by ``build()`` into the git-ignored
+``baseline/_ref``) on this host's cores over the FULL tensor of the same
+workload: a few outer iterations (the ones actually run are printed), init row
+excluded, no scaling.  Under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -132,39 +134,125 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU side ------
-def cpu_slab(dims, target_elems=1 << 28):
-    """Leading modes kept, last mode cut so the slab holds ~2^28 elements (2 GiB)."""
-    lead = math.prod(dims[:-1])
-    last = max(1, min(dims[-1], target_elems // lead))
-    return tuple(dims[:-1]) + (last,)
+def cpu_info():
+    """(model name, usable host cores) of this box."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count()
+    return model, cores
 
 
-def cpu_reference_time(conf, steps, warmup):
-    """Time the oracle port (numpy/OpenBLAS, all host threads) on a slab; s/iter scaled to the full tensor."""
+def host_tensor(conf):
+    """The config's synthetic tensor as a host float64 array (flat, mode-1 fastest).
+
+    With a GPU present it is generated by the same seeded generator as the GPU
+    arm (identical bits) and copied down; input preparation only, never timed."""
+    import torch
+
+    dims, R = conf["dims"], conf["rank"]
+    if torch.cuda.is_available():
+        from paper_1909_01149_b200.synth import synthetic_block, truth_factors
+
+        fs = truth_factors(dims, R, DATA_SEED, conf["kind"])
+        xd = synthetic_block(dims, fs, conf["eta"], DATA_SEED)
+        host = torch.empty(xd.numel(), dtype=torch.float64)
+        chunk = 1 << 28
+        for k in range(0, xd.numel(), chunk):          # bounded staging, no second device copy
+            host[k:k + chunk].copy_(xd[k:k + chunk])
+        del xd
+        torch.cuda.empty_cache()
+        return host.numpy(), "seeded generator of the GPU arm (same bits), copied to host"
+    from oracle import nncp_oracle as O   # CPU-only box: same distribution, host-built
+
+    rng = np.random.default_rng(DATA_SEED)
+    hs = [rng.random((d, R)) for d in dims]
+    x = O.khatri_rao(hs) @ np.ones(R)
+    x += conf["eta"] * float(np.sqrt(np.mean(x * x))) * np.abs(rng.standard_normal(x.size))
+    return x, "host numpy generator (no GPU)"
+
+
+def reference_steps(dims, steps, warmup):
+    """(timed, warm-up) outer iterations the reference arm runs: everything requested for
+    tensors the CPU finishes quickly, 2 + 1 at >= 2^28 elements (each 2048^3 iteration is
+    tens of seconds on the host)."""
+    if math.prod(dims) >= 1 << 28:
+        return max(1, min(steps, 2)), 1
+    if math.prod(dims) >= 1 << 24:
+        return max(1, min(steps, 5)), min(warmup, 2)
+    return steps, warmup
+
+
+def reference_arm(conf, steps, warmup):
+    """The UNMODIFIED reference ``nncp_sequential`` (driver.py:495-505) on the full tensor.
+
+    The reference is pure Python + numpy/OpenBLAS; ``build()`` installs it into the
+    git-ignored ``baseline/_ref`` (pip --target from /root/reference).  Timed: the mean
+    of ``RunReport.row_wall`` over the iterations after the warm-up; the init row (its
+    einsum MTTKRP) runs but is excluded, as BASELINE.md §2 specifies.  Falls back to
+    the oracle port when baseline/_ref is missing."""
+    dims, R = conf["dims"], conf["rank"]
+    k, w = reference_steps(dims, steps, warmup)
+    data, src = host_tensor(conf)
+    model, cores = cpu_info()
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    kind = "reference"
+    if os.path.isdir(os.path.join(ref_dir, "nncp")):
+        sys.path.insert(0, ref_dir)
+        import nncp
+
+        t0 = time.perf_counter()
+        rep = nncp.nncp_sequential(nncp.DenseTensor(dims, data),
+                                   nncp.RunConfig(rank=R, algorithm=conf["algo"], max_iters=w + k, tol=0.0,
+                                                  seed=INIT_SEED))
+        total = time.perf_counter() - t0
+        walls = list(rep.row_wall)
+        mttkrp = [row["MTTKRP"] for row in rep.rows]
+        what = "unmodified reference nncp_sequential (baseline/_ref, numpy + OpenBLAS)"
+    else:
+        from oracle import nncp_oracle as O
+
+        kind = "port"
+        walls = []
+        t0 = time.perf_counter()
+        O.run_sequential(data, dims, R, conf["algo"], max_iters=w + k, tol=0.0, seed=INIT_SEED, timings=walls)
+        total = time.perf_counter() - t0
+        mttkrp = None
+        what = "oracle port of the reference (baseline/_ref not installed)"
+    timed = walls[1 + w:]
+    t = statistics.mean(timed)
+    info = {"value": t, "unit": "s/iter", "cores": cores, "kind": kind, "cpu_model": model,
+            "sample": (f"{what} on the full {'x'.join(map(str, dims))} tensor ({src}); "
+                       f"{len(timed)} timed outer iterations after {w} warm-up, init row excluded "
+                       f"({walls[0]:.1f} s), no scaling"),
+            "init_row_s": walls[0], "iteration_s": timed, "total_wall_s": total}
+    if mttkrp is not None:
+        info["mttkrp_s"] = statistics.mean(mttkrp[1 + w:])
+    return info, k, w
+
+
+def cpu_baseline_port(host, conf):
+    """Our arm's bounded CPU baseline: ONE outer iteration of the oracle port (numpy +
+    OpenBLAS, all host threads) on the full host tensor of the e2e leg (init skipped)."""
     from oracle import nncp_oracle as O
 
-    dims, rank = conf["dims"], conf["rank"]
-    slab = cpu_slab(dims)
-    rng = np.random.default_rng(DATA_SEED)
-    hs = [rng.random((d, rank)) for d in slab]
-    # sum of rank-one terms built slice by slice (no 2^28 x R Khatri-Rao temporary)
-    lead = math.prod(slab[:-1])
-    krp_lead = O.khatri_rao(hs[:-1])                     # (prod of leading dims, R)
-    data = np.empty(math.prod(slab))
-    for k in range(slab[-1]):
-        data[k * lead:(k + 1) * lead] = krp_lead @ hs[-1][k]
-    rms = float(np.sqrt(np.mean(data * data)))
-    data += conf["eta"] * rms * np.abs(rng.standard_normal(data.size))
-    timings = []
-    O.run_sequential(data, slab, rank, conf["algo"], max_iters=warmup + steps, tol=0.0, seed=INIT_SEED,
-                     timings=timings, init_error="tree")
-    per_iter = timings[1 + warmup:]
-    scale = math.prod(dims) / math.prod(slab)
-    t = statistics.mean(per_iter) * scale
-    cores = os.cpu_count()
-    sample = (f"{len(per_iter)} outer iterations of the oracle port on a {'x'.join(map(str, slab))} slab "
-              f"(same leading modes), s/iter scaled by I/I_slab = {scale:.1f}; init row excluded")
-    return t, cores, sample
+    dims, R = conf["dims"], conf["rank"]
+    model, cores = cpu_info()
+    walls = []
+    O.run_sequential(host, dims, R, conf["algo"], max_iters=1, tol=0.0, seed=INIT_SEED, timings=walls,
+                     init_error="none")
+    return {"value": walls[1], "unit": "s/iter", "cores": cores, "kind": "port", "cpu_model": model,
+            "sample": (f"1 outer iteration of the oracle port (numpy + OpenBLAS, {cores} threads) on the full "
+                       f"{'x'.join(map(str, dims))} tensor, init skipped, no scaling")}
 
 
 # ------------------------------------------------------------ GPU side ------
@@ -202,7 +290,10 @@ def gpu_run(args, conf):
     coll = DistCollectives(layout) if world > 1 else IdentityCollectives()
     cfg = P.RunConfig(rank=R, algorithm=conf["algo"], max_iters=args.warmup + args.steps + 1, tol=0.0,
                       seed=INIT_SEED, cuda_graph=False if args.eager else None)
-    eng = _Engine(x_local, layout.local_dims, dims, cfg, coll, layout if world > 1 else None, timing=False)
+    # timing=True: the per-category CUDA events are event-record nodes of the replayed
+    # sweep graph, so the timed region itself yields the breakdown (and the partials'
+    # per-launch times); they cost ~1 us each
+    eng = _Engine(x_local, layout.local_dims, dims, cfg, coll, layout if world > 1 else None, timing=True)
     clocks = ClockSampler(dev)
     clocks.start()
     eng.initialise()
@@ -213,9 +304,10 @@ def gpu_run(args, conf):
             dist.barrier()
         torch.cuda.synchronize()
 
-    eng.ctx.kernel_events = []
     launches0 = _lib.load().nncp_launch_count()
     replays0 = eng.graph_replays
+    eng.timer.tags = {}
+    rows0 = len(eng.report.rows)
     barrier()
     clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -229,25 +321,19 @@ def gpu_run(args, conf):
     launches = _lib.load().nncp_launch_count() - launches0
     launches += (eng.graph_replays - replays0) * eng.graph_kernels   # kernel nodes replayed by the sweep graph
     dev_s = e0.elapsed_time(e1) / 1e3
-    kev = eng.ctx.kernel_events
-    if not kev:
-        # graph replay records no per-kernel events: time the same kernels in 2 eager sweeps
-        eng.graph, graph = None, eng.graph
-        eng.cfg.cuda_graph = False
-        eng.cfg.max_iters += 2
-        eng.iterate(2)
-        torch.cuda.synchronize()
-        kev = eng.ctx.kernel_events
-    eng.ctx.kernel_events = None
-    k_left = [a.elapsed_time(b) / 1e3 for side, a, b in kev if side == "left"]
-    k_right = [a.elapsed_time(b) / 1e3 for side, a, b in kev if side == "right"]
-    t = torch.tensor([dev_s, sum(k_left), sum(k_right)], dtype=torch.float64, device="cuda")
+    rows = eng.report.rows[rows0:]
+    cats = {c: sum(r[c] for r in rows) / max(1, len(rows)) for c in P.CATEGORIES}
+    tags = eng.timer.tags
+    n_left, n_right = tags.get("partial_left", [0.0, 0])[1], tags.get("partial_right", [0.0, 0])[1]
+    t = torch.tensor([dev_s, tags.get("partial_left", [0.0])[0], tags.get("partial_right", [0.0])[0]],
+                     dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_s, kl_sum, kr_sum = t.tolist()
     errors = list(eng.report.errors)
-    out = dict(dev_s=dev_s, wall=wall, k_left=kl_sum / max(1, len(k_left)), k_right=kr_sum / max(1, len(k_right)),
-               n_left=len(k_left), n_right=len(k_right), clocks=clk, launches=int(launches), errors=errors,
+    out = dict(dev_s=dev_s, wall=wall, k_left=kl_sum / max(1, n_left), k_right=kr_sum / max(1, n_right),
+               n_left=n_left, n_right=n_right, clocks=clk, launches=int(launches), errors=errors,
+               categories=cats, graph=eng.graph is not None,
                local_dims=layout.local_dims, grid=grid, world=world, rank=rank, split=eng.plan.split,
                levels=eng.sliced.levels if eng.sliced is not None else None)
     # ------------------------------------------------------- e2e leg ----------
@@ -285,6 +371,8 @@ def gpu_run(args, conf):
     out["h2d_bytes"] = int(host.numel() * 8)
     out["d2h_bytes"] = int(sum(m.size for m in model) * 8 + lam.size * 8 + 16 * args.steps)
     out["e2e_errors"] = list(rep2.errors)
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu"] = cpu_baseline_port(host.numpy(), conf)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -319,12 +407,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        t, cores, sample = cpu_reference_time(conf, max(1, min(args.steps, 3)), 1)
+        info, k, w = reference_arm(conf, args.steps, args.warmup)
+        t = info["value"]
         line = {"metric": METRIC, "impl": "reference", "value": t, "unit": "s/iter", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False,
+                "steps": k, "warmup": w, "steps_requested": args.steps, "warmup_requested": args.warmup,
+                "ms_per_step": t * 1e3, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config,
-                "cpu_baseline": {"value": t, "unit": "s/iter", "cores": cores, "kind": "port", "sample": sample},
+                "cpu_baseline": info,
                 "e2e": {"value": t, "unit": "s/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -383,13 +473,13 @@ def main():
         traffic = tr.get(key, {}).get("dram_bytes_per_launch")
     roofline["traffic"] = traffic
     mttkrp_tflops = 4.0 * local_size * R / mttkrp_s / 1e12 if mttkrp_s > 0 else None
-    cpu = None
-    if res["world"] == 1 and not args.no_cpu_baseline:
-        try:
-            t, cores, sample = cpu_reference_time(conf, 2, 1)
-            cpu = {"value": t, "unit": "s/iter", "cores": cores, "kind": "port", "sample": sample}
-        except MemoryError:
-            cpu = None
+    # per-category device time of the timed iterations (CUDA events captured in the sweep
+    # graph); "host_gap" = the rest of ms_per_step: the per-iteration eps read-back and
+    # graph launch between two replays
+    breakdown = {c: v * 1e3 for c, v in res["categories"].items() if v > 0}
+    breakdown["attributed"] = sum(res["categories"].values()) * 1e3
+    breakdown["host_gap"] = s_iter * 1e3 - breakdown["attributed"]
+    cpu = res.get("cpu")
     line = {
         "metric": METRIC, "value": s_iter, "unit": "s/iter", "n_gpus": res["world"], "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": s_iter * 1e3, "higher_is_better": False, "scaling": "strong",
@@ -400,7 +490,10 @@ def main():
         "mttkrp_vs_fp64_roofline": t_fp64_roof / mttkrp_s if mttkrp_s > 0 else None,
         "mttkrp_roofline_frac": (t_sliced_roof / mttkrp_s if t_sliced_roof else t_fp64_roof / mttkrp_s)
         if mttkrp_s > 0 else None,
-        "partial_ms": {"left": res["k_left"] * 1e3, "right": res["k_right"] * 1e3},
+        "partial_ms": {"left": res["k_left"] * 1e3, "right": res["k_right"] * 1e3,
+                       "source": "event-record nodes around each partial inside the replayed sweep graph, "
+                                 "timed region"},
+        "breakdown_ms": breakdown,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": res["e2e_s"] / args.steps, "unit": "s/iter",

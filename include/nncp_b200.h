@@ -75,8 +75,11 @@ size_t nncp_workspace_bytes(int order, const int64_t* dims, int split, int rank)
 
 /* tensor_ops.py:76-78 norm_squared: out[0] = sum x^2 (deterministic reduction). */
 int nncp_norm_squared(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
-/* Same sum (bitwise), plus out_min[0] = min x in the same pass: the negative-entry
- * UserWarning of driver.py:571-573 without a second read of the tensor.  n >= 1. */
+/* Same sum (bitwise), plus in the same pass (out_min: 3 doubles): out_min[0] = min x,
+ * the negative-entry UserWarning of driver.py:571-573 without a second read of the
+ * tensor; out_min[1] = max |x| (NaN if any entry is NaN or +-Inf); out_min[2] = the
+ * smallest nonzero |x| (+Inf if none) -- the sign / dynamic-range facts the engine's
+ * "auto" MTTKRP choice needs before slicing the tensor.  n >= 1. */
 int nncp_norm_squared_min(const double* x, int64_t n, double* out_sum, double* out_min, void* ws, size_t ws_bytes,
                           void* stream);
 
@@ -159,6 +162,14 @@ int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, s
 /* driver.py:368,431 gamma = lam^T (prod_m sym(G_m)) lam over all `order` Grams. */
 int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma,
                void* stream);
+/* The same gamma, plus the end-of-sweep status hand-off (grid.py:172-203 failure
+ * propagation).  codes[0..nslots) is a rank-slotted vector: every slot is zeroed, then
+ * for n < count codes[offset + n] = kind * 2^32 + failing row of status n (0 when the
+ * update succeeded; exact in fp64) and masks_out[2n..2n+1] = its warning bits (may be
+ * NULL); then status n is reset (replaces nncp_status_reset_n inside a sweep).  One
+ * SUM All-Reduce of `codes` then gives every rank every rank's failures. */
+int nncp_gamma_publish(const double* grams, int order, int rank, const double* lam, double* gamma_out, int* status,
+                       int count, double* codes, int nslots, int offset, int* masks_out, void* stream);
 
 /* tensor_ops.py:208-212 matrix_inner_product <a, b * lam> (lam may be NULL). */
 int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank,

@@ -397,13 +397,16 @@ def run_sequential(data, dims, rank, algorithm="bpp", max_iters=100, tol=1e-6, s
     tree = DimTree(dims, rank, strict_split) if use_dimtree else None
     duals = [None] * order          # ADMM state per mode (updaters.py:56-68)
     centres = [None] * order        # Nesterov proximal centre per mode
-    if init_error == "naive":
-        m0 = naive_mttkrp(data, dims, hs, order - 1)
-    else:  # same quantity through the tree's last-mode path (bench baseline: init is not timed)
-        m0 = DimTree(dims, rank, strict_split).mttkrp_last_mode(data, hs)
-    beta0 = float(np.dot(m0.ravel(), (hs[-1] * lam).ravel()))
-    gamma0 = float(lam @ (np.prod(grams, axis=0) @ lam))
-    errors = [eps_from_terms(alpha, beta0, gamma0)]
+    if init_error == "none":   # bench baseline only: the init row is not timed, skip its MTTKRP
+        errors = [float("nan")]
+    else:
+        if init_error == "naive":
+            m0 = naive_mttkrp(data, dims, hs, order - 1)
+        else:  # same quantity through the tree's last-mode path
+            m0 = DimTree(dims, rank, strict_split).mttkrp_last_mode(data, hs)
+        beta0 = float(np.dot(m0.ravel(), (hs[-1] * lam).ravel()))
+        gamma0 = float(lam @ (np.prod(grams, axis=0) @ lam))
+        errors = [eps_from_terms(alpha, beta0, gamma0)]
     if timings is not None:
         timings.append(time.perf_counter() - t0)
     for it in range(1, max_iters + 1):

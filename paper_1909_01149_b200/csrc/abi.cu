@@ -31,6 +31,7 @@ int update(int, const double*, int, int, int, const double*, const double*, cons
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
+int gamma_publish(const double*, int, int, const double*, double*, int*, int, double*, int, int, int*, cudaStream_t);
 int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
 int status_reset(int*, int, cudaStream_t);
@@ -252,6 +253,16 @@ int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, s
 int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma_out, void* stream) {
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
   return gamma(grams, order, rank, lam, gamma_out, S(stream));
+}
+
+int nncp_gamma_publish(const double* grams, int order, int rank, const double* lam, double* gamma_out, int* status,
+                       int count, double* codes, int nslots, int offset, int* masks_out, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  if (!status || !codes) return fail(NNCP_ERR_VALUE, "status and codes buffers required");
+  if (count < 0 || count > kMaxOrder) return fail(NNCP_ERR_VALUE, "status count must be in [0, max order]");
+  if (offset < 0 || offset + count > nslots) return fail(NNCP_ERR_VALUE, "status slot outside the codes vector");
+  return gamma_publish(grams, order, rank, lam, gamma_out, status, count, codes, nslots, offset, masks_out,
+                       S(stream));
 }
 
 int nncp_inner(const double* a, const double* b, const double* lam, int64_t rows, int rank, double* out, void* ws,

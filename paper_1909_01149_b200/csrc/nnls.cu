@@ -386,7 +386,8 @@ __global__ void __launch_bounds__(256)
 // ------------------------------------------------------------- scalars -----
 __global__ void __launch_bounds__(256)
     gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
-                 double* __restrict__ gamma) {
+                 double* __restrict__ gamma, int* status = nullptr, int count = 0, double* codes = nullptr,
+                 int nslots = 0, int offset = 0, int* masks = nullptr) {
   __shared__ double W[kMaxRank * kMaxRank];
   __shared__ double v[kMaxRank];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -411,6 +412,27 @@ __global__ void __launch_bounds__(256)
     for (int k = 0; k < R; ++k) s = fma(lam[k], v[k], s);
     gamma[0] = s;
   }
+  // end of sweep: publish this context's update status and reset it for the next sweep
+  // (the reset the caller would otherwise launch separately).  codes[0..nslots) is the
+  // rank-slotted vector that one SUM All-Reduce combines: every slot is zeroed, then
+  // this rank's slot [offset, offset + count) gets, per mode, failure kind * 2^32 +
+  // failing row (0 = none; exact in fp64); masks[2n..2n+1] = the warning bits.
+  if (status == nullptr) return;
+  for (int e = threadIdx.x; e < nslots; e += blockDim.x) codes[e] = 0.0;
+  __syncthreads();
+  if (threadIdx.x < count) {
+    int* st = status + threadIdx.x * NNCP_STATUS_WORDS;
+    const int kind = st[3], row = st[2];
+    codes[offset + threadIdx.x] = kind ? double(kind) * 4294967296.0 + double(row) : 0.0;
+    if (masks != nullptr) {
+      masks[2 * threadIdx.x] = st[0];
+      masks[2 * threadIdx.x + 1] = st[1];
+    }
+    st[0] = 0;
+    st[1] = 0;
+    st[2] = INT_MAX;
+    st[3] = 0;
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -429,45 +451,88 @@ __global__ void __launch_bounds__(256)
   if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, 1, out);
 }
 
-// out[0] = sum x^2 (fixed-order reduction); with out_min, also out_min[0] = min x in
-// the same pass (the reference's negative-entry warning, driver.py:571-573).
+// out[0] = sum x^2 (fixed-order reduction); with out_min, in the same pass:
+// out_min[0] = min x (the reference's negative-entry warning, driver.py:571-573),
+// out_min[1] = max |x| and out_min[2] = min over the nonzero |x| (INFINITY if none):
+// the dynamic range the sliced MTTKRP engine's "auto" choice checks.
+__device__ __forceinline__ void minmax_acc(double v, double& mn, double& amax, double& anz) {
+  const double a = fabs(v);
+  mn = fmin(mn, v);
+  amax = fmax(amax, a);
+  anz = fmin(anz, a > 0.0 ? a : INFINITY);
+}
+
 __global__ void __launch_bounds__(512)
     norm_sq_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part, double* out,
                    double* out_min, unsigned int* ticket) {
   __shared__ double red[16];
-  __shared__ double redm[16];
-  double s0 = 0.0, s1 = 0.0, mn = INFINITY;
+  __shared__ double redm[3][16];
+  double s0 = 0.0, s1 = 0.0, mn = INFINITY, amax = 0.0, anz = INFINITY;
   const int64_t n2 = n / 2;
   const double2* x2 = reinterpret_cast<const double2*>(x);
+  bool nonfinite = false;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n2; e += int64_t(gridDim.x) * blockDim.x) {
     const double2 v = __ldcs(x2 + e);
     s0 = fma(v.x, v.x, s0);
     s1 = fma(v.y, v.y, s1);
-    mn = fmin(mn, fmin(v.x, v.y));
+    if (out_min != nullptr) {
+      minmax_acc(v.x, mn, amax, anz);
+      minmax_acc(v.y, mn, amax, anz);
+      nonfinite |= !isfinite(v.x) || !isfinite(v.y);
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
     s0 = fma(x[n - 1], x[n - 1], s0);
-    mn = fmin(mn, x[n - 1]);
+    minmax_acc(x[n - 1], mn, amax, anz);
+    nonfinite |= !isfinite(x[n - 1]);
   }
+  // fmin/fmax drop NaN: a non-finite entry poisons the max so callers can see it
+  if (nonfinite) amax = NAN;
   const double s = block_sum(s0 + s1, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
   if (out_min != nullptr) {
+    bool bad = nonfinite;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = mn;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      anz = fmin(anz, __shfl_xor_sync(0xffffffffu, anz, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+      redm[0][threadIdx.x >> 5] = mn;
+      redm[1][threadIdx.x >> 5] = bad ? NAN : amax;
+      redm[2][threadIdx.x >> 5] = anz;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double m = redm[0];
-      for (int w = 1; w < int(blockDim.x >> 5); ++w) m = fmin(m, redm[w]);
+      double m = redm[0][0], a = redm[1][0], z = redm[2][0];
+      bool nan = isnan(a);
+      for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        m = fmin(m, redm[0][w]);
+        nan |= isnan(redm[1][w]);
+        a = fmax(a, redm[1][w]);
+        z = fmin(z, redm[2][w]);
+      }
       part[gridDim.x + blockIdx.x] = m;
+      part[2 * gridDim.x + blockIdx.x] = nan ? NAN : a;
+      part[3 * gridDim.x + blockIdx.x] = z;
     }
   }
   if (last_cta_ticket(ticket)) {
     finish_partials(part, gridDim.x, 1, out);
     if (out_min != nullptr && threadIdx.x == 0) {
-      double m = part[gridDim.x];
-      for (int b = 1; b < int(gridDim.x); ++b) m = fmin(m, part[gridDim.x + b]);
+      double m = part[gridDim.x], a = part[2 * gridDim.x], z = part[3 * gridDim.x];
+      bool nan = isnan(a);
+      for (int b = 1; b < int(gridDim.x); ++b) {
+        m = fmin(m, part[gridDim.x + b]);
+        nan |= isnan(part[2 * gridDim.x + b]);
+        a = fmax(a, part[2 * gridDim.x + b]);
+        z = fmin(z, part[3 * gridDim.x + b]);
+      }
       out_min[0] = m;
+      out_min[1] = nan ? NAN : a;
+      out_min[2] = z;
     }
   }
 }
@@ -568,6 +633,13 @@ int gamma(const double* grams, int order, int rank, const double* lam, double* o
   return NNCP_OK;
 }
 
+int gamma_publish(const double* grams, int order, int rank, const double* lam, double* out, int* status, int count,
+                  double* codes, int nslots, int offset, int* masks, cudaStream_t st) {
+  gamma_kernel<<<1, 256, 0, st>>>(grams, order, rank, lam, out, status, count, codes, nslots, offset, masks);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
 int inner(const double* a, const double* b, const double* lam, int64_t rows, int rank, double* out, void* ws,
           size_t ws_bytes, cudaStream_t st) {
   WsLayout w = ws_layout(ws, ws_bytes);
@@ -583,7 +655,7 @@ int norm_squared(const double* x, int64_t n, double* out, double* out_min, void*
                  cudaStream_t st) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n / 2 + 511) / 512, int64_t(num_sms()) * 8)));
-  if (w.part_elems < size_t(blocks) * (out_min ? 2 : 1)) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
+  if (w.part_elems < size_t(blocks) * (out_min ? 4 : 1)) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
   if (reinterpret_cast<uintptr_t>(x) % 16) return fail(NNCP_ERR_VALUE, "tensor must be 16-byte aligned");
   if (out_min != nullptr && n < 1) return fail(NNCP_ERR_VALUE, "min of an empty tensor");
   norm_sq_kernel<<<blocks, 512, 0, st>>>(x, n, w.part, out, out_min, w.tickets + T_NORM);

@@ -22,6 +22,7 @@ Category seconds come from CUDA events on the launching stream.
 from __future__ import annotations
 
 import math
+import os
 import threading
 import time
 import warnings
@@ -36,7 +37,7 @@ from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, Ran
                    ThreadGrid, block_partition)
 from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
 from .updaters import (AdmmRunner, BppCyclingError, NesterovRunner, _SPack,  # noqa: F401
-                       raise_for_status)
+                       raise_for_code, raise_for_status, warn_for_status)
 
 __all__ = ["ALGORITHMS", "CATEGORIES", "RunConfig", "RunReport", "init_factor", "nncp_parallel",
            "nncp_sequential", "record_category", "relative_error", "IN_SCOPE_ALGORITHMS", "run_local"]
@@ -186,7 +187,10 @@ class _EventTimer:
         self._marks = []
         self._start = None
         self.capturing = False          # marks become event-record nodes of the sweep graph
-        self.graph_marks = None         # (start, [(category, event), ...]) of the captured sweep
+        self.graph_marks = None         # (start, [(category, tag, event), ...]) of the captured sweep
+        # tag -> [seconds, count]: finer intervals inside a category (e.g. each partial
+        # MTTKRP launch, "partial_left" / "partial_right"), accumulated like the rows
+        self.tags = {}
 
     def _event(self):
         if self.capturing:
@@ -210,9 +214,17 @@ class _EventTimer:
         if not self.enabled or self.graph_marks is None:
             return
         prev, marks = self.graph_marks
-        for cat, e in marks:
-            row[cat] += prev.elapsed_time(e) / 1e3
+        for cat, tag, e in marks:
+            dt = prev.elapsed_time(e) / 1e3
+            row[cat] += dt
+            self._tag(tag, dt)
             prev = e
+
+    def _tag(self, tag, dt):
+        if tag is not None:
+            acc = self.tags.setdefault(tag, [0.0, 0])
+            acc[0] += dt
+            acc[1] += 1
 
     def start(self):
         if not self.enabled:
@@ -221,20 +233,24 @@ class _EventTimer:
         self._start.record()
         self._marks = []
 
-    def mark(self, category):
+    def mark(self, category, tag=None):
+        """Close the interval since the previous mark and attribute it to ``category``
+        (and, when given, to ``tag``)."""
         if not self.enabled:
             return
         e = self._event()
         e.record()
-        self._marks.append((category, e))
+        self._marks.append((category, tag, e))
 
     def collect(self, row: dict):
         """Accumulate (after the stream is synchronised) into ``row``."""
         if not self.enabled or self._start is None:
             return
         prev = self._start
-        for cat, e in self._marks:
-            row[cat] += prev.elapsed_time(e) / 1e3
+        for cat, tag, e in self._marks:
+            dt = prev.elapsed_time(e) / 1e3
+            row[cat] += dt
+            self._tag(tag, dt)
             self._pool.append(prev)
             prev = e
         self._pool.append(prev)
@@ -253,12 +269,68 @@ SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
 _HBM_BPS, _DMMA_FLOPS, _SLICED_BPS, _SLICED_FIXED_S = 6.45e12, 37.1e12, 6.9e12, 5e-5
 
 
-def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6, extra_bytes: int = 0) -> bool:
+# "auto" slices only tensors whose nonzero magnitudes span at most this ratio: the digit
+# planes keep 46 bits relative to each row's maximum, so an entry 2^k below it keeps
+# 46 - k bits ("Engine choice")
+SLICED_MAX_RANGE = 2.0 ** 10
+
+
+class TensorFacts:
+    """What the initial norm pass learns about the local tensor (one read, nncp_norm_squared_min)."""
+
+    __slots__ = ("alpha", "min", "absmax", "absmin_nz")
+
+    def __init__(self, alpha, xmin, absmax, absmin_nz):
+        self.alpha, self.min, self.absmax, self.absmin_nz = float(alpha), float(xmin), float(absmax), float(absmin_nz)
+
+    @property
+    def finite(self) -> bool:
+        return math.isfinite(self.alpha) and math.isfinite(self.absmax)
+
+    @property
+    def signed(self) -> bool:
+        return self.min < 0.0
+
+    @property
+    def dynamic_range(self) -> float:
+        if self.absmax == 0.0 or not math.isfinite(self.absmin_nz):
+            return 1.0
+        return self.absmax / self.absmin_nz
+
+
+def _sliced_ok_for(facts: TensorFacts, algorithm: str):
+    """Why "auto" must not slice this tensor (None = it may).  The Ozaki-scheme bound of
+    the sliced engine is relative to row / column-chunk maxima, not to each output: with
+    cancellation (signed tensors, or UCP's signed factors) or entries far below their
+    row's maximum the relative error of an output can exceed the 1e-12 MTTKRP tolerance
+    (tests/test_gpu_sliced.py::test_auto_engine_guards); non-finite entries have no digits."""
+    if facts is None:
+        return None
+    if not facts.finite:
+        return "non-finite entries"
+    if facts.signed:
+        return "negative entries"
+    if algorithm == "ucp":
+        return "signed (unconstrained) factors"
+    if facts.dynamic_range > SLICED_MAX_RANGE:
+        return f"nonzero magnitudes span {facts.dynamic_range:.3g}x"
+    return None
+
+
+def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6, extra_bytes: int = 0,
+                facts: TensorFacts = None, algorithm: str = "hals") -> bool:
     """Resolve RunConfig.mttkrp_kernel for one execution context."""
     if kind == "fp64":
         return False
+    if facts is not None and not facts.finite:
+        if kind == "sliced":
+            warnings.warn("tensor has non-finite entries; the sliced MTTKRP engine cannot represent them, "
+                          "using the fp64 engine")
+        return False
     if kind == "sliced":
         return True
+    if _sliced_ok_for(facts, algorithm) is not None:
+        return False
     size = int(np.prod(dims))
     if size < SLICED_MIN_ELEMS:
         return False
@@ -271,11 +343,13 @@ def _use_sliced(kind: str, dims, split: int, rank: int, dev, levels: int = 6, ex
     return SlicedTensor.nbytes(dims, split, levels) + SLICED_HBM_MARGIN + extra_bytes <= free
 
 
-def _engine_plan(dims, cfg: RunConfig, dev, extra_bytes: int = 0):
+def _engine_plan(dims, cfg: RunConfig, dev, extra_bytes: int = 0, facts: TensorFacts = None):
     """Dimension-tree plan and partial-MTTKRP engine of one execution context:
-    (plan, sliced?).  ``extra_bytes``: device memory still to be allocated first."""
+    (plan, sliced?).  ``extra_bytes``: device memory still to be allocated first;
+    ``facts``: sign / range of the tensor (None before it is on the device)."""
     plan = DimTreePlan.create(dims, int(cfg.rank), cfg.strict_split)
-    if not _use_sliced(cfg.mttkrp_kernel, dims, plan.split, int(cfg.rank), dev, cfg.mttkrp_levels, extra_bytes):
+    if not _use_sliced(cfg.mttkrp_kernel, dims, plan.split, int(cfg.rank), dev, cfg.mttkrp_levels, extra_bytes,
+                       facts, cfg.algorithm):
         return plan, False
     if cfg.dimtree_split == "auto":
         s_bal = choose_balanced_split(dims)
@@ -299,6 +373,25 @@ def _reserve_sliced(dims, cfg: RunConfig):
 def _split_rows(dims, s: int) -> int:
     """M + J of the root split S: the rows of the two partial outputs and of the Khatri-Rao digit sides."""
     return math.prod(dims[:s]) + math.prod(dims[s:])
+
+
+def first_failure(vec, nranks: int, order: int):
+    """(mode, kind, row) of the first failed update in an All-Reduced hand-off vector
+    ``[beta, code(rank 0, mode 0..N-1), code(rank 1, ...), ...]`` (nncp_gamma_publish):
+    lowest mode first, then lowest rank -- every rank reads the same vector, so every
+    rank raises the same error (grid.py:172-203 re-raises one worker's exception)."""
+    for n in range(order):
+        for r in range(nranks):
+            code = int(vec[1 + r * order + n])
+            if code:
+                return n, code >> 32, code & 0xFFFFFFFF
+    return None
+
+
+# test hook: "rank:iteration:mode:kind:row" makes that rank's update report a failure
+# (kind 1 = BppCyclingError, 2 = singular) so the cross-rank hand-off can be exercised
+# on real kernels; eager sweeps only.  Never set outside tests.
+_FAULT_ENV = "NNCP_TEST_INJECT_FAULT"
 
 
 class _Engine:
@@ -326,7 +419,25 @@ class _Engine:
             self.slice_rows = list(layout.slice_rows)
             self.owned_parts = list(layout.owned_parts)
         self.n_owned = [s.stop - s.start for s in self.owned_rows]
-        self.plan, use_sliced = _engine_plan(self.dims, cfg, dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.lib = _lib.load()
+        self.report = RunReport()
+        self.timer = _EventTimer(timing)
+        self._wall0 = time.perf_counter()
+        # init row (driver.py:338-345): ||X||^2 of the local block, in the same read also
+        # min x (negative-entry warning), max |x| and the smallest nonzero |x| -- the facts
+        # the "auto" MTTKRP engine choice needs before the tensor is sliced
+        self.scal = torch.zeros(7, **f64)     # beta, gamma, alpha, beta0, min x, max |x|, min nonzero |x|
+        self.timer.start()
+        norm_ws = Workspace(1 << 20)
+        _lib.check(self.lib.nncp_norm_squared_min(_lib.ptr(x_local), x_local.numel(),
+                                                  _lib.vp(self.scal.data_ptr() + 16),
+                                                  _lib.vp(self.scal.data_ptr() + 32), norm_ws.ptr, norm_ws.nbytes,
+                                                  _lib.stream_handle()))
+        self.timer.mark("Error")
+        sc = self.scal.tolist()
+        self.facts = TensorFacts(sc[2], sc[4], sc[5], sc[6])
+        self.plan, use_sliced = _engine_plan(self.dims, cfg, dev, facts=self.facts)
         self.sliced = None
         if use_sliced:
             self.sliced = SlicedTensor(x_local, self.dims, self.plan.split, cfg.mttkrp_levels)
@@ -335,15 +446,28 @@ class _Engine:
             ws_bytes = max(ws_bytes, self.plan.sliced_workspace_bytes(self.sliced.levels))
         self.ws = Workspace(ws_bytes)
         self.ctx = DimTreeContext(self.plan, workspace=self.ws, sliced=self.sliced)
-        f64 = dict(dtype=torch.float64, device=dev)
+        # partials -> "MTTKRP", TTVs -> "MultiTTV" (the reference's recorder, dimtree.py:209-233)
+        self.ctx.marker = self.timer.mark if timing else None
         R, N = self.R, self.N
         self.grams = torch.zeros((N, R, R), **f64)
         self.lam = torch.ones(R, **f64)
         self.nsq = torch.zeros(R, **f64)
-        self.scal = torch.zeros(5, **f64)           # beta, gamma, alpha, beta0, min x (warn_negative)
         # driver.py:571-573: the negative-entry warning, from the initial norm pass
         self.warn_negative = bool(warn_negative) and cfg.algorithm != "ucp"
         self.status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32, device=dev)
+        _lib.check(self.lib.nncp_status_reset_n(_lib.ptr(self.status), N, _lib.stream_handle()))
+        # end-of-sweep hand-off (grid.py:172-203): [beta, failure code per (rank, mode)].
+        # The last update writes beta into slot 0, nncp_gamma_publish zeroes the code slots,
+        # writes this rank's and resets the status words; ONE SUM All-Reduce (the
+        # reference's beta All-Reduce, driver.py:429) then gives every rank every failure,
+        # so all ranks raise the same error in the same iteration instead of one rank
+        # leaving the others blocked in the next collective.
+        self.nranks = layout.grid.total if layout is not None else 1
+        self.me = layout.rank if layout is not None else 0
+        self.xvec = torch.zeros(1 + self.nranks * N, **f64)
+        self.masks = torch.zeros(2 * N, dtype=torch.int32, device=dev)
+        fault = os.environ.get(_FAULT_ENV)
+        self.fault = tuple(int(v) for v in fault.split(":")) if fault else None
         self.mbar = torch.empty((max(self.dims), R), **f64)
         self.hhat = torch.empty((max(max(self.n_owned), 1), R), **f64)
         self.owned = [torch.empty((self.n_owned[n], R), **f64) for n in range(N)]
@@ -352,9 +476,8 @@ class _Engine:
         else:
             self.shared = self.owned
         self.host_scal = torch.zeros(2, dtype=torch.float64).pin_memory()
-        self.host_status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32).pin_memory()
-        self.timer = _EventTimer(timing)
-        self.lib = _lib.load()
+        self.host_xvec = torch.zeros(1 + self.nranks * N, dtype=torch.float64).pin_memory()
+        self.host_masks = torch.zeros(2 * N, dtype=torch.int32).pin_memory()
         # stateful rules (updaters.py:56-68): per-mode ADMM dual / Nesterov centre
         rows_max = max(max(self.n_owned), 1)
         if cfg.algorithm in ("admm", "nes"):
@@ -372,7 +495,6 @@ class _Engine:
         self.graph_failed = False
         self.graph_kernels = 0      # library kernels captured in the sweep graph
         self.graph_replays = 0
-        self.report = RunReport()
 
     # -- small wrappers -------------------------------------------------------
     def _st(self):
@@ -386,21 +508,12 @@ class _Engine:
     def initialise(self):
         lib, st, R = self.lib, self._st(), self.R
         self.report.begin_row()
-        wall0 = time.perf_counter()
-        self.timer.start()
-        if self.warn_negative:
-            _lib.check(lib.nncp_norm_squared_min(_lib.ptr(self.x), self.x.numel(),
-                                                 _lib.vp(self.scal.data_ptr() + 16),
-                                                 _lib.vp(self.scal.data_ptr() + 32), self.ws.ptr, self.ws.nbytes, st))
-        else:
-            _lib.check(lib.nncp_norm_squared(_lib.ptr(self.x), self.x.numel(), _lib.vp(self.scal.data_ptr() + 16),
-                                             self.ws.ptr, self.ws.nbytes, st))
-        self.timer.mark("Error")
+        wall0 = self._wall0          # the norm pass ran in __init__ (it picks the engine)
         alpha_t = self.scal[2:3]
         self.coll.all_reduce(alpha_t)
         self.timer.mark("AllReduce")
         self.alpha = float(alpha_t.item())
-        if self.warn_negative and float(self.scal[4].item()) < 0.0:
+        if self.warn_negative and self.facts.signed:
             warnings.warn("tensor has negative entries; nonnegative model will not fit")
         if self.alpha <= 0.0:
             raise ValueError("zero tensor has no relative error")
@@ -457,7 +570,6 @@ class _Engine:
         cfg = self.cfg
         if cfg.use_dimtree:
             self.ctx.begin_iteration()
-        _lib.check(lib.nncp_status_reset_n(_lib.ptr(self.status), N, st))
         for n in range(N):
             mb = self.mbar[: self.dims[n]]
             if cfg.use_dimtree:
@@ -472,11 +584,14 @@ class _Engine:
                 _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
                                            _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
                                            _lib.ptr(self.hhat), _lib.ptr(self.nsq),
-                                           _lib.ptr(self.scal) if last else None, _lib.ptr(self.status[n]),
+                                           _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]),
                                            self.ws.ptr, self.ws.nbytes, st))
             else:
                 self._iterative_update(n, m_owned, last)
             self.timer.mark("NNLS")
+            if self.fault is not None and self.fault[:3] == (self.me, len(self.report.errors), n):
+                self.status[n, 3] = self.fault[3]
+                self.status[n, 2] = self.fault[4]
             self.coll.all_reduce(self.nsq)
             self.timer.mark("AllReduce")
             _lib.check(lib.nncp_normalize_gram(_lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R,
@@ -487,12 +602,16 @@ class _Engine:
             self.timer.mark("AllReduce")
             self._gather(n)
             self.timer.mark("AllGather")
-        self.coll.all_reduce(self.scal[0:1])
+        _lib.check(lib.nncp_gamma_publish(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam),
+                                          _lib.vp(self.scal.data_ptr() + 8), _lib.ptr(self.status), N,
+                                          _lib.vp(self.xvec.data_ptr() + 8), self.nranks * N, self.me * N,
+                                          _lib.ptr(self.masks), st))
+        self.timer.mark("Error")
+        self.coll.all_reduce(self.xvec, words=1)      # beta + every rank's status codes
         self.timer.mark("AllReduce")
-        _lib.check(lib.nncp_gamma(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam), _lib.vp(self.scal.data_ptr() + 8),
-                                  st))
+        self.host_xvec.copy_(self.xvec, non_blocking=True)
         self.host_scal.copy_(self.scal[0:2], non_blocking=True)
-        self.host_status.copy_(self.status, non_blocking=True)
+        self.host_masks.copy_(self.masks, non_blocking=True)
         self.timer.mark("Error")
 
     def _hook(self, t, op):
@@ -507,7 +626,8 @@ class _Engine:
         spack = _SPack(self.grams, self.N, n)
         try:
             if self.cfg.algorithm == "admm":
-                x, _ = self.runner.run(spack, m_owned, cur, self.admm_dual[n], self._hook, status=self.status[n])
+                x, _ = self.runner.run(spack, m_owned, cur, self.admm_dual[n], self._hook, status=self.status[n],
+                                       defer_errors=True)
             else:
                 xstar = self.nes_prev[n] if self.nes_prev[n] is not None else cur
                 x, _ = self.runner.run(spack, m_owned, cur, xstar, self._hook)
@@ -520,7 +640,7 @@ class _Engine:
         hh.copy_(x[:rows])
         _lib.check(lib.nncp_colsumsq(_lib.ptr(hh), rows, R, _lib.ptr(self.nsq), self.ws.ptr, self.ws.nbytes, st))
         if last:
-            _lib.check(lib.nncp_inner(_lib.ptr(m_owned), _lib.ptr(hh), None, rows, R, _lib.ptr(self.scal),
+            _lib.check(lib.nncp_inner(_lib.ptr(m_owned), _lib.ptr(hh), None, rows, R, _lib.ptr(self.xvec),
                                       self.ws.ptr, self.ws.nbytes, st))
 
     # -- Nesterov outer extrapolation (driver.py:452-492) ----------------------------
@@ -588,14 +708,18 @@ class _Engine:
 
     def _finish_iteration(self, it):
         torch.cuda.current_stream().synchronize()
-        status = self.host_status.tolist()
+        masks = self.host_masks.tolist()
         for n in range(self.N):
+            warn_for_status(masks[2 * n], masks[2 * n + 1], self.cfg.algorithm)
+        vec = self.host_xvec.tolist()
+        fail = first_failure(vec, self.nranks, self.N)
+        if fail is not None:
+            n, kind, row = fail
             try:
-                raise_for_status(status[n], self.cfg.algorithm)
+                raise_for_code(kind, row)
             except Exception as exc:
                 raise RuntimeError(f"NNLS update failed at iteration {it}, mode {n + 1}") from exc
-        beta, gamma = self.host_scal.tolist()
-        return _eps_from_terms(self.alpha, beta, gamma)
+        return _eps_from_terms(self.alpha, vec[0], self.host_scal[1].item())
 
     def iterate(self, count: int = None):
         """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
@@ -603,7 +727,7 @@ class _Engine:
         errors = self.report.errors
         capturable = ((not self.coll.parallel or getattr(self.coll, "capturable", False))
                       and cfg.algorithm in FUSED_ALGORITHMS)
-        use_graph = capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))
+        use_graph = (capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))) and self.fault is None
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
         for it in range(done + 1, stop + 1):
@@ -723,11 +847,22 @@ def nncp_parallel(x: DenseTensor, cfg: RunConfig) -> RunReport:
     rank returns the merged report.  Otherwise the grid is simulated by worker
     threads on the local GPU with rank-ordered, bitwise-reproducible
     collectives (the reference's execution model, grid.py:172-203).
+
+    ``x`` is a DenseTensor (host, pinned, memory-mapped or device-resident) or
+    the path of an NNCP tensor file; every rank copies only its own block
+    (driver.py:233-236): from a file it reads just the block's byte ranges,
+    from a device tensor it slices in HBM, from host memory it copies the block.
     """
-    cfg.validate(x.order)
+    if isinstance(x, (str, os.PathLike)):
+        from .tensor_io import read_tensor_dims
+
+        dims = read_tensor_dims(x)
+    else:
+        dims = x.dims
+    cfg.validate(len(dims))
     if cfg.grid is None:
         raise ValueError("parallel driver needs a grid shape")
-    for n, (i, p) in enumerate(zip(x.dims, cfg.grid)):
+    for n, (i, p) in enumerate(zip(dims, cfg.grid)):
         if p > i:
             raise ValueError(f"grid dim {p} exceeds tensor dim {i} in mode {n + 1}; "
                              "every worker must hold a nonempty tensor block")
@@ -735,11 +870,27 @@ def nncp_parallel(x: DenseTensor, cfg: RunConfig) -> RunReport:
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() == grid.total:
-        return _parallel_dist(x, cfg, grid)
+        return _parallel_dist(x, dims, cfg, grid)
+    if isinstance(x, (str, os.PathLike)):
+        from .tensor_io import read_tensor
+
+        x = read_tensor(x)
     return _parallel_threads(x, cfg, grid)
 
 
-def _local_block(x: DenseTensor, layout: RankLayout) -> torch.Tensor:
+def local_block(x, layout: RankLayout) -> torch.Tensor:
+    """This rank's tensor block in HBM, flat and mode-1 fastest, never materialising
+    more than the block on the host: file -> byte-range reads; device tensor -> a
+    slice copy in HBM; host array -> the block's elements only."""
+    offs = [s.start for s in layout.slice_rows]
+    if isinstance(x, (str, os.PathLike)):
+        from .tensor_io import read_tensor_block
+
+        return as_device(read_tensor_block(x, offs, layout.local_dims))
+    if x.on_device:
+        # reversed-dims C view of the F-ordered buffer: index [i_N, ..., i_1]
+        view = x.data.view(tuple(reversed(x.dims)))
+        return view[tuple(reversed(layout.slice_rows))].contiguous().view(-1)
     arr = x.as_array()[tuple(layout.slice_rows)]
     return as_device(np.asarray(arr).ravel(order="F"))
 
@@ -749,17 +900,16 @@ def _parallel_threads(x: DenseTensor, cfg: RunConfig, grid: Grid) -> RunReport:
     results = [None] * grid.total
     failures = [None] * grid.total
     dev = torch.cuda.current_device()
-    hostx = DenseTensor(x.dims, x.host_data())
-    _warn_if_negative(hostx, cfg)
+    _warn_if_negative(x, cfg)
 
     def main(rank):
         try:
             torch.cuda.set_device(dev)
             layout = RankLayout(grid, rank, x.dims)
-            xl = _local_block(hostx, layout)
             coll = ThreadCollectives(tgrid, layout)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
+                xl = local_block(x, layout)       # on the worker's stream, ahead of its kernels
                 eng, rep = run_local(xl, layout.local_dims, x.dims, cfg, coll, layout)
                 owned, lam = eng.model_host()
             results[rank] = (rep, owned, lam, layout.owned_rows)
@@ -780,20 +930,27 @@ def _parallel_threads(x: DenseTensor, cfg: RunConfig, grid: Grid) -> RunReport:
     return _merge_reports(results, x.dims, cfg.rank)
 
 
-def _parallel_dist(x: DenseTensor, cfg: RunConfig, grid: Grid) -> RunReport:
+def _parallel_dist(x, dims, cfg: RunConfig, grid: Grid) -> RunReport:
     import torch.distributed as dist
 
     rank = dist.get_rank()
-    layout = RankLayout(grid, rank, x.dims)
+    layout = RankLayout(grid, rank, dims)
     coll = DistCollectives(layout)
-    xl = _local_block(DenseTensor(x.dims, x.host_data()), layout)
-    if rank == 0:
-        _warn_if_negative(x, cfg)
-    eng, rep = run_local(xl, layout.local_dims, x.dims, cfg, coll, layout)
+    xl = local_block(x, layout)
+    if cfg.algorithm != "ucp":
+        # driver.py:571-573 over the whole tensor: min of the blocks (an init-time
+        # reduction outside the reference's counted collectives)
+        lo = torch.min(xl).reshape(1).to(torch.float64)
+        if coll.stage:
+            lo = lo.cpu()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        if rank == 0 and float(lo.item()) < 0.0:
+            warnings.warn("tensor has negative entries; nonnegative model will not fit")
+    eng, rep = run_local(xl, layout.local_dims, dims, cfg, coll, layout)
     owned, lam = eng.model_host()
     gathered = [None] * grid.total
     dist.all_gather_object(gathered, (rep, owned, lam, layout.owned_rows))
-    return _merge_reports(gathered, x.dims, cfg.rank)
+    return _merge_reports(gathered, dims, cfg.rank)
 
 
 def _merge_reports(results, dims, rank) -> RunReport:

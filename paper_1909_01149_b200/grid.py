@@ -201,7 +201,7 @@ class IdentityCollectives:
     def __init__(self):
         self.counters = CommCounters()
 
-    def all_reduce(self, t, op="sum"):
+    def all_reduce(self, t, op="sum", words=None):
         if op not in ("sum", "max", "min"):
             raise ValueError(f"unknown reduction {op!r}")
         return t
@@ -243,7 +243,9 @@ class DistCollectives:
             dist_groups = make_slice_process_groups(grid)
         self.slice_pg = [dist_groups[n][c] for n, c in enumerate(layout.coord)]
 
-    def all_reduce(self, t, op="sum"):
+    def all_reduce(self, t, op="sum", words=None):
+        """``words``: the payload the reference's call carries when ``t`` also carries
+        piggy-backed internal words (the status codes on beta's All-Reduce)."""
         ops = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}
         if op not in ops:
             raise ValueError(f"unknown reduction {op!r}")
@@ -253,7 +255,8 @@ class DistCollectives:
             t.copy_(h)
         else:
             self.dist.all_reduce(t, op=ops[op])
-        self.counters.record("AllReduce", t.numel(), t.numel())
+        w = t.numel() if words is None else int(words)
+        self.counters.record("AllReduce", w, w)
         return t
 
     def reduce_scatter(self, mode, t, parts):
@@ -377,7 +380,7 @@ class ThreadCollectives:
     def _sync():
         torch.cuda.current_stream().synchronize()
 
-    def all_reduce(self, t, op="sum"):
+    def all_reduce(self, t, op="sum", words=None):
         if op not in ("sum", "max", "min"):
             raise ValueError(f"unknown reduction {op!r}")
         self._sync()
@@ -396,7 +399,8 @@ class ThreadCollectives:
 
         out = self.tgrid.all_rv.exchange(self.layout.rank, t, combine)
         t.copy_(out)
-        self.counters.record("AllReduce", t.numel(), t.numel())
+        w = t.numel() if words is None else int(words)
+        self.counters.record("AllReduce", w, w)
         return t
 
     def reduce_scatter(self, mode, t, parts):

@@ -26,6 +26,7 @@ from .tensor_ops import Workspace, as_device
 __all__ = ["UpdateInputs", "UpdaterState", "BppCyclingError", "mu_update", "hals_update", "bpp_update",
            "ucp_update", "admm_update", "nesterov_update", "default_admm_rho", "nesterov_hyperparams",
            "MU_EPSILON", "BPP_BACKUP_TRIES", "ADMM_INNER_CAP", "NESTEROV_INNER_CAP", "raise_for_status",
+           "raise_for_code", "warn_for_status",
            "local_reduce", "AdmmRunner", "NesterovRunner"]
 
 ADMM_INNER_CAP = 5        # updaters.py:25
@@ -77,15 +78,31 @@ class UpdaterState:
     last_inner_iters: int = 0
 
 
-def raise_for_status(status_host, algo: str = "hals"):
-    """Translate kernel status words into the reference's warnings / exceptions."""
-    mask = (int(status_host[0]) & 0xFFFFFFFF) | ((int(status_host[1]) & 0xFFFFFFFF) << 32)
+def warn_for_status(mask_lo, mask_hi, algo: str = "hals"):
+    """The reference's per-update warnings (updaters.py:84,112) from the status mask words."""
+    mask = (int(mask_lo) & 0xFFFFFFFF) | ((int(mask_hi) & 0xFFFFFFFF) << 32)
     if algo == "hals" and mask:
         for r in range(64):
             if (mask >> r) & 1:
                 warnings.warn(f"zero gram diagonal in column {r}, skipping")
     if algo == "ucp" and mask & 1:
         warnings.warn("singular gram in unconstrained update, adding ridge")
+
+
+def raise_for_code(kind: int, row: int):
+    """The reference's NNLS exceptions (updaters.py:87-88,152,163) from a failure kind / row."""
+    if kind == 1:
+        raise BppCyclingError(int(row))
+    if kind == 2:
+        raise torch.linalg.LinAlgError("Singular matrix")  # numpy.linalg.LinAlgError analogue
+    if kind == 3:
+        raise NotImplementedError("gram singular even with the ridge; the reference's lstsq fallback "
+                                  "(updaters.py:87-88) is not on the device path")
+
+
+def raise_for_status(status_host, algo: str = "hals"):
+    """Translate kernel status words into the reference's warnings / exceptions."""
+    warn_for_status(status_host[0], status_host[1], algo)
     kind = int(status_host[3])
     if kind == 1:
         raise BppCyclingError(int(status_host[2]))
@@ -183,7 +200,10 @@ class AdmmRunner:
         self.rows, self.rank = rows, rank
 
     def run(self, spack: _SPack, m: torch.Tensor, current: torch.Tensor, u: torch.Tensor, hook, rho=None,
-            max_steps: int = ADMM_INNER_CAP, rtol: float = 1e-4, status=None):
+            max_steps: int = ADMM_INNER_CAP, rtol: float = 1e-4, status=None, defer_errors: bool = False):
+        """``defer_errors``: leave a failed solve in ``status`` instead of raising here, so
+        every rank keeps issuing the same hook All-Reduces; the engine raises the same
+        error on every rank after the sweep (grid.py:172-203)."""
         lib = _lib.load()
         st = _lib.stream_handle()
         status = self.status if status is None else status
@@ -203,9 +223,10 @@ class AdmmRunner:
             red = hook(self.sums[:5], "sum")
             host = red.detach().cpu().numpy() if isinstance(red, torch.Tensor) else np.asarray(red)
             rho_used = float(self.sums[5].item())
-            stv = status.cpu().tolist()
-            if int(stv[3]):
-                raise_for_status(stv, "admm")
+            if not defer_errors:
+                stv = status.cpu().tolist()
+                if int(stv[3]):
+                    raise_for_status(stv, "admm")
             gap, nx, nxhat, step, nu = np.sqrt(host)
             if gap <= rtol * max(nx, nxhat) and rho_used * step <= rtol * nu * rho_used:
                 break

@@ -291,3 +291,89 @@ def test_sliced_balanced_split_grid_run(P):
     assert np.max(np.abs(np.array(par.errors) - np.array(errors))) <= TRACE_TOL
     for a, b in zip(par.model.factors, factors):
         assert np.max(np.abs(a - b)) <= FACTOR_TOL
+
+
+def _heavy_tailed(rng, dims, r, spikes=32):
+    """Nonnegative rows with a few 2^20 spikes in slices where the contracted factor is zero:
+    the outputs never see the spikes, but the row scale of the digit planes does."""
+    x = rng.uniform(0.5, 1.0, int(np.prod(dims))).reshape(dims[2], -1)
+    cols = rng.choice(dims[2], size=spikes, replace=False)
+    x[cols, :] = 2.0 ** 20
+    hs = [rng.random((d, r)) for d in dims]
+    hs[2][cols, :] = 0.0
+    return x.ravel(), hs
+
+
+def _cancelling(rng, dims, r, k):
+    """Signed rows x[m, j] = s_j (1 + 2^-k u): with factor rows equal in pairs and s_j
+    alternating, the O(1) parts cancel exactly and the outputs are O(2^-k)."""
+    m = int(np.prod(dims[:2]))
+    s = np.where(np.arange(dims[2]) % 2 == 0, 1.0, -1.0)
+    x = (s[:, None] * (1.0 + 2.0 ** -k * rng.random((dims[2], m)))).ravel()
+    hs = [rng.random((d, r)) for d in dims]
+    hs[2][1::2] = hs[2][0::2]
+    return x, hs
+
+
+def test_sliced_six_levels_failure_modes(P):
+    """Where the 6-level Ozaki bound (relative to each row's maximum) does NOT give 1e-12
+    on the outputs -- the cases "auto" routes to the fp64 engine: heavy-tailed rows whose
+    spikes meet zero factor rows, and signed rows whose large parts cancel.  The fp64
+    engine meets the tolerance on the same inputs."""
+    dims, r = (64, 64, 4096), 16
+    plan = P.DimTreePlan.create(dims, r)
+    rng = np.random.default_rng(77)
+    for name, (x, hs) in (("heavy-tailed", _heavy_tailed(rng, dims, r)),
+                          ("cancelling", _cancelling(rng, dims, r, 10))):
+        xd = P.DenseTensor(dims, x).to_device()
+        want = O.partial_left(x, dims, plan.split, hs)
+        fp64 = rel_fro(_np(P.partial_mttkrp(xd, hs, "left", plan).data), want)
+        sl6 = rel_fro(_np(P.partial_mttkrp(xd, hs, "left", plan, sliced=_sliced(P, xd, plan, 6)).data), want)
+        print(f"{name}: fp64 {fp64:.2e}  sliced-6 {sl6:.2e}")
+        assert fp64 <= MTTKRP_TOL, (name, fp64)
+        assert sl6 > MTTKRP_TOL, (name, sl6)   # the failure mode the engine choice guards against
+
+
+@pytest.mark.parametrize("case", ["signed", "heavy-tailed", "ucp", "nonneg"])
+def test_auto_engine_guards(P, case):
+    """mttkrp_kernel="auto" at a size where the cost model picks the sliced engine:
+    it slices only finite, nonnegative tensors of moderate dynamic range, and never for
+    UCP's signed factors (driver._sliced_ok_for)."""
+    from paper_1909_01149_b200.driver import _Engine
+    from paper_1909_01149_b200.grid import IdentityCollectives
+
+    dims, r = (512, 512, 256), 32                # 2^26 elements: sliced wins the cost model
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0.5, 1.0, int(np.prod(dims)))
+    algo = "hals"
+    if case == "signed":
+        x[::1000] = -1e-3
+    elif case == "heavy-tailed":
+        x[::100000] = 1e6
+    elif case == "ucp":
+        algo = "ucp"
+    xd = P.DenseTensor(dims, x).to_device()
+    eng = _Engine(xd.data, dims, dims, P.RunConfig(rank=r, algorithm=algo, max_iters=1), IdentityCollectives())
+    sliced = eng.sliced is not None
+    assert sliced == (case == "nonneg"), (case, eng.facts.min, eng.facts.dynamic_range)
+    if case == "signed":
+        assert eng.facts.signed
+    del eng, xd
+
+
+def test_non_finite_tensor_uses_fp64_engine(P):
+    """NaN / Inf have no digits: even a forced sliced engine falls back (with a warning) and
+    the NaN propagates into the error trace like the reference's arithmetic."""
+    import torch
+
+    from paper_1909_01149_b200.driver import _Engine
+    from paper_1909_01149_b200.grid import IdentityCollectives
+
+    dims, r = (40, 30, 20), 4
+    x = np.random.default_rng(2).random(int(np.prod(dims)))
+    x[123] = np.nan
+    xd = torch.as_tensor(x, device="cuda")
+    with pytest.warns(UserWarning, match="non-finite"):
+        eng = _Engine(xd, dims, dims, P.RunConfig(rank=r, algorithm="hals", max_iters=1, mttkrp_kernel="sliced"),
+                      IdentityCollectives())
+    assert eng.sliced is None and not eng.facts.finite

@@ -150,3 +150,70 @@ def test_nccl_sweep_graph_capture_matches_eager_and_sequential():
             assert np.array_equal(a, b) and np.array_equal(a, c), name
         assert cg == ce, (name, cg, ce)
         assert cg["calls"]["AllReduce"] > 0
+
+
+def _fault_worker(rank, world, port, out_q):
+    """Rank 1's mode-2 update in iteration 2 reports BPP cycling (row 7): every rank must
+    raise the same wrapped error in the same iteration, none may block in a collective."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["NNCP_TEST_INJECT_FAULT"] = "1:2:1:1:7"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1909_01149_b200 as P
+        from tests.conftest import load_golden
+
+        g = load_golden("runs.npz")
+        dims = tuple(int(d) for d in g["bpp3_dims"])
+        x = P.DenseTensor(dims, g["bpp3_x"])
+        try:
+            P.nncp_parallel(x, P.RunConfig(rank=4, algorithm="bpp", max_iters=5, tol=0.0, grid=(2, 1, 1)))
+            out_q.put((rank, "no error"))
+        except RuntimeError as exc:
+            cause = exc.__cause__
+            out_q.put((rank, (str(exc), type(cause).__name__, getattr(cause, "column", None))))
+    except Exception as exc:  # noqa: BLE001
+        out_q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_spmd_failure_on_one_rank_raises_everywhere():
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fault_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(2))      # a hang would time out here
+    for p in procs:
+        p.join(timeout=120)
+    for k in range(2):
+        assert out[k] == ("NNLS update failed at iteration 2, mode 2", "BppCyclingError", 7), (k, out[k])
+
+
+def test_thread_grid_failure_on_one_worker_raises(golden, monkeypatch):
+    """The same hand-off in the thread-simulated grid (rank-ordered device reductions)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1909_01149_b200 as P
+    from paper_1909_01149_b200.updaters import BppCyclingError
+
+    monkeypatch.setenv("NNCP_TEST_INJECT_FAULT", "3:1:2:1:4")
+    g = golden("runs.npz")
+    dims = tuple(int(d) for d in g["bpp3_dims"])
+    with pytest.raises(RuntimeError, match="iteration 1, mode 3") as info:
+        P.nncp_parallel(P.DenseTensor(dims, g["bpp3_x"]),
+                        P.RunConfig(rank=4, algorithm="bpp", max_iters=3, tol=0.0, grid=(2, 2, 1)))
+    assert isinstance(info.value.__cause__, BppCyclingError) and info.value.__cause__.column == 4
