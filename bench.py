@@ -276,8 +276,12 @@ def gpu_run(args, conf):
     backend = os.environ.get("NNCP_DIST_BACKEND", "nccl")
     dev = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(dev)
+    nccl_env = None
     if world > 1:
         if backend == "nccl":
+            from paper_1909_01149_b200.grid import pin_nccl_environment
+
+            nccl_env = pin_nccl_environment(debug=True)     # init lines on stderr: rank count per comm
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
@@ -333,7 +337,8 @@ def gpu_run(args, conf):
     errors = list(eng.report.errors)
     out = dict(dev_s=dev_s, wall=wall, k_left=kl_sum / max(1, n_left), k_right=kr_sum / max(1, n_right),
                n_left=n_left, n_right=n_right, clocks=clk, launches=int(launches), errors=errors,
-               categories=cats, graph=eng.graph is not None,
+               categories=cats, graph=eng.graph is not None, nccl_env=nccl_env,
+               merged_norm_gram=eng.merge_norm_gram,
                local_dims=layout.local_dims, grid=grid, world=world, rank=rank, split=eng.plan.split,
                levels=eng.sliced.levels if eng.sliced is not None else None)
     # ------------------------------------------------------- e2e leg ----------
@@ -503,6 +508,8 @@ def main():
                         "through the engine): tensor H2D once per call of "
                         f"{args.steps} iterations + init + D2H of the model, divided by the steps"},
         "gpu_launches": res["launches"],
+        "collectives": ({"backend": "nccl", "env": res["nccl_env"], "merged_norm_gram": res["merged_norm_gram"]}
+                        if res["world"] > 1 else None),
         "clocks": res["clocks"],
         "final_error": res["errors"][-1],
     }

@@ -159,6 +159,13 @@ int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int
 int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, size_t ws_bytes,
               void* stream);
 
+/* driver.py:411-422 from the All-Reduced Gram of the UNnormalised rows (one collective
+ * instead of the norm and Gram All-Reduces): w = sqrt(diag(gram_raw)),
+ * owned = hhat / (w > 0 ? w : 1), lam = w, gram = sym(gram_raw) / (w' w'^T).
+ * gram must not alias gram_raw. */
+int nncp_normalize_from_gram(const double* hhat, const double* gram_raw, int64_t rows, int rank, double* owned,
+                             double* lam, double* gram, void* stream);
+
 /* driver.py:368,431 gamma = lam^T (prod_m sym(G_m)) lam over all `order` Grams. */
 int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma,
                void* stream);

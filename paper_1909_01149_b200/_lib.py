@@ -70,6 +70,7 @@ SIGNATURES = [
      [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gram", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gamma", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    ("nncp_normalize_from_gram", ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
     ("nncp_gamma_publish", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int,
                                           ctypes.c_int, vp, vp]),
     ("nncp_inner", ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),

@@ -31,6 +31,7 @@ int update(int, const double*, int, int, int, const double*, const double*, cons
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
+int normalize_from_gram(const double*, const double*, int64_t, int, double*, double*, double*, cudaStream_t);
 int gamma_publish(const double*, int, int, const double*, double*, int*, int, double*, int, int, int*, cudaStream_t);
 int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
@@ -253,6 +254,14 @@ int nncp_gram(const double* h, int64_t rows, int rank, double* gram, void* ws, s
 int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma_out, void* stream) {
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
   return gamma(grams, order, rank, lam, gamma_out, S(stream));
+}
+
+int nncp_normalize_from_gram(const double* hhat, const double* gram_raw, int64_t rows, int rank, double* owned,
+                             double* lam, double* gram, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  if (!gram_raw) return fail(NNCP_ERR_VALUE, "raw gram required");
+  if (gram == gram_raw) return fail(NNCP_ERR_VALUE, "gram output must not alias the raw gram");
+  return normalize_from_gram(hhat, gram_raw, rows, rank, owned, lam, gram, S(stream));
 }
 
 int nncp_gamma_publish(const double* grams, int order, int rank, const double* lam, double* gamma_out, int* status,

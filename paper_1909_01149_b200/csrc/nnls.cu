@@ -383,6 +383,32 @@ __global__ void __launch_bounds__(256)
   if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, RR, gram);
 }
 
+// Normalisation from the All-Reduced Gram of the UNnormalised rows (the grid path's
+// merged collective): nsq = diag(G^), w = sqrt(nsq) (driver.py:411-418),
+// H = H^ / (w > 0 ? w : 1), lam = w, and the Gram of the normalised factor
+// G = sym(G^) / (w' w'^T) (driver.py:419-422) without a second pass over the rows.
+__global__ void __launch_bounds__(256)
+    normalize_from_gram_kernel(const double* __restrict__ hhat, const double* __restrict__ graw, int64_t rows,
+                               int R, double* __restrict__ owned, double* __restrict__ lam,
+                               double* __restrict__ gram) {
+  __shared__ double scale[kMaxRank];
+  if (threadIdx.x < R) {
+    const double w = sqrt(graw[threadIdx.x * R + threadIdx.x]);
+    scale[threadIdx.x] = (w > 0.0) ? w : 1.0;
+    if (blockIdx.x == 0 && lam) lam[threadIdx.x] = w;
+  }
+  __syncthreads();
+  const int64_t n = rows * R;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    owned[e] = hhat[e] / scale[int(e % R)];
+  if (blockIdx.x == 0 && gram) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int a = e / R, b = e - (e / R) * R;
+      gram[e] = 0.5 * (graw[a * R + b] + graw[b * R + a]) / (scale[a] * scale[b]);
+    }
+  }
+}
+
 // ------------------------------------------------------------- scalars -----
 __global__ void __launch_bounds__(256)
     gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
@@ -623,6 +649,15 @@ int normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank
   NNCP_RP_CASES(rp, (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
                                                                       owned, lam, gram, w.part,
                                                                       w.tickets + ticket_slot)));
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+int normalize_from_gram(const double* hhat, const double* graw, int64_t rows, int rank, double* owned, double* lam,
+                        double* gram, cudaStream_t st) {
+  const int64_t n = std::max<int64_t>(rows, 0) * rank;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 4)));
+  normalize_from_gram_kernel<<<blocks, 256, 0, st>>>(hhat, graw, std::max<int64_t>(rows, 0), rank, owned, lam, gram);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

@@ -452,6 +452,9 @@ class _Engine:
         self.grams = torch.zeros((N, R, R), **f64)
         self.lam = torch.ones(R, **f64)
         self.nsq = torch.zeros(R, **f64)
+        # grid runs over NCCL: norm + Gram All-Reduces merged into one (DistCollectives)
+        self.merge_norm_gram = bool(getattr(coll, "merge_norm_gram", False))
+        self.graw = torch.zeros((R, R), **f64) if self.merge_norm_gram else None
         # driver.py:571-573: the negative-entry warning, from the initial norm pass
         self.warn_negative = bool(warn_negative) and cfg.algorithm != "ucp"
         self.status = torch.zeros((N, _lib.STATUS_WORDS), dtype=torch.int32, device=dev)
@@ -592,14 +595,26 @@ class _Engine:
             if self.fault is not None and self.fault[:3] == (self.me, len(self.report.errors), n):
                 self.status[n, 3] = self.fault[3]
                 self.status[n, 2] = self.fault[4]
-            self.coll.all_reduce(self.nsq)
-            self.timer.mark("AllReduce")
-            _lib.check(lib.nncp_normalize_gram(_lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R,
-                                               _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
-                                               _lib.ptr(self.grams[n]), self.ws.ptr, self.ws.nbytes, st))
-            self.timer.mark("Gram")
-            self.coll.all_reduce(self.grams[n])
-            self.timer.mark("AllReduce")
+            if self.merge_norm_gram:
+                # one All-Reduce of the unnormalised Gram: its diagonal is nsq
+                _lib.check(lib.nncp_gram(_lib.ptr(self.hhat), self.n_owned[n], R, _lib.ptr(self.graw),
+                                         self.ws.ptr, self.ws.nbytes, st))
+                self.timer.mark("Gram")
+                self.coll.all_reduce(self.graw)
+                self.timer.mark("AllReduce")
+                _lib.check(lib.nncp_normalize_from_gram(_lib.ptr(self.hhat), _lib.ptr(self.graw), self.n_owned[n],
+                                                        R, _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
+                                                        _lib.ptr(self.grams[n]), st))
+                self.timer.mark("NNLS")
+            else:
+                self.coll.all_reduce(self.nsq)
+                self.timer.mark("AllReduce")
+                _lib.check(lib.nncp_normalize_gram(_lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R,
+                                                   _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
+                                                   _lib.ptr(self.grams[n]), self.ws.ptr, self.ws.nbytes, st))
+                self.timer.mark("Gram")
+                self.coll.all_reduce(self.grams[n])
+                self.timer.mark("AllReduce")
             self._gather(n)
             self.timer.mark("AllGather")
         _lib.check(lib.nncp_gamma_publish(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam),

@@ -23,6 +23,7 @@ entering the call, words_out = elements leaving it.
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -30,7 +31,7 @@ import numpy as np
 import torch
 
 __all__ = ["block_partition", "DistMap", "CommCounters", "Group", "Grid", "IdentityCollectives",
-           "DistCollectives", "ThreadCollectives", "ThreadGrid"]
+           "DistCollectives", "ThreadCollectives", "ThreadGrid", "pin_nccl_environment"]
 
 
 def block_partition(length: int, parts: int) -> "DistMap":
@@ -225,7 +226,7 @@ class DistCollectives:
 
     parallel = True
 
-    def __init__(self, layout: RankLayout, dist_groups=None):
+    def __init__(self, layout: RankLayout, dist_groups=None, merge_norm_gram=None):
         import torch.distributed as dist
 
         self.dist = dist
@@ -238,6 +239,15 @@ class DistCollectives:
         # (kernels + collectives) can be captured as one CUDA graph; the
         # host-staged gloo path cannot.
         self.capturable = not self.stage
+        # Per mode, the column norms and the Gram of the normalised factor come from ONE
+        # All-Reduce of the unnormalised Gram (diag = nsq) instead of the
+        # reference's two (driver.py:414,421): N fewer latency-bound collectives per sweep,
+        # counted as what is sent.  Default on NCCL grids of > 1 rank; the gloo path keeps
+        # the reference's schedule (and counters) unless NNCP_MERGE_NORM_GRAM=1.
+        env = os.environ.get("NNCP_MERGE_NORM_GRAM")
+        if merge_norm_gram is None:
+            merge_norm_gram = (env == "1") if env is not None else (not self.stage and dist.get_world_size() > 1)
+        self.merge_norm_gram = bool(merge_norm_gram)
         grid = layout.grid
         if dist_groups is None:
             dist_groups = make_slice_process_groups(grid)
@@ -314,6 +324,26 @@ class DistCollectives:
             res = out
         self.counters.record("AllGather", t.numel(), res.numel())
         return res
+
+
+# Collective determinism (grid.py:242-262 reduces in rank order, bitwise reproducible;
+# SPEC.md:390-391): NCCL is run-to-run deterministic for a fixed algorithm / protocol /
+# topology, so the grid path pins them instead of letting the tuner switch with message
+# size.  Ring + LL: defined for all three collectives, lowest latency for the <= 1 MB
+# messages of the NNCP sweep.  Set before the communicators are created; explicit user
+# settings win.
+NCCL_PINS = {"NCCL_ALGO": "Ring", "NCCL_PROTO": "LL"}
+
+
+def pin_nccl_environment(debug: bool = False) -> dict:
+    """setdefault NCCL_ALGO / NCCL_PROTO (and NCCL_DEBUG=INFO for the INIT subsystem when
+    ``debug``: communicator-init lines that show the rank count); returns what is in effect."""
+    for k, v in NCCL_PINS.items():
+        os.environ.setdefault(k, v)
+    if debug:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return {k: os.environ.get(k) for k in list(NCCL_PINS) + ["NCCL_DEBUG"]}
 
 
 def make_slice_process_groups(grid: Grid):

@@ -38,6 +38,8 @@ def _worker(rank, world, port, case, out_q):
         g = load_golden("runs.npz")
         name, grid = case[:2]
         engine = case[2] if len(case) > 2 else "auto"
+        if len(case) > 3 and case[3] == "merged":
+            os.environ["NNCP_MERGE_NORM_GRAM"] = "1"
         dims = tuple(int(d) for d in g[f"{name}_dims"])
         r, iters, iseed = (int(v) for v in g[f"{name}_meta"])
         algo = str(g[f"{name}_algo"])
@@ -55,7 +57,8 @@ def _worker(rank, world, port, case, out_q):
 
 
 @pytest.mark.parametrize("case", [("hals_odd", (2, 2, 1)), ("mu4", (2, 1, 2, 1)), ("bpp3", (2, 2, 2)),
-                                  ("bpp3", (2, 2, 2), "sliced"), ("mu4", (2, 1, 2, 1), "sliced")])
+                                  ("bpp3", (2, 2, 2), "sliced"), ("mu4", (2, 1, 2, 1), "sliced"),
+                                  ("bpp3", (2, 2, 2), "auto", "merged"), ("hals_odd", (2, 2, 1), "auto", "merged")])
 def test_spmd_processes_match_reference_grid_run(golden, case):
     import torch
     import torch.multiprocessing as mp
@@ -82,8 +85,16 @@ def test_spmd_processes_match_reference_grid_run(golden, case):
         for n, f in enumerate(factors):
             assert np.max(np.abs(f - g[f"{tag}_f{n}"])) <= 1e-6
         # merged counters: the reference's per-worker collective calls summed over workers
-        if str(g[f"{name}_algo"]) != "hals":
-            assert calls == list(g[f"{tag}_calls"])
+        want = list(g[f"{tag}_calls"])
+        if len(case) > 3 and case[3] == "merged":
+            # one All-Reduce per mode and sweep instead of two (norms + Gram), every worker
+            r, iters, _ = (int(v) for v in g[f"{name}_meta"])
+            want[2] -= world * len(grid) * iters
+            if str(g[f"{name}_algo"]) == "hals":   # the reference's discarded per-column hook calls
+                want[2] -= world * len(grid) * r * iters
+            assert calls == want, (calls, want)
+        elif str(g[f"{name}_algo"]) != "hals":
+            assert calls == want
 
 
 def _nccl_graph_worker(port, out_q):
