@@ -51,7 +51,8 @@ extern "C" {
 #define NNCP_ALGO_MU 1        /* updaters.py:91-94   */
 #define NNCP_ALGO_HALS 2      /* updaters.py:97-118  */
 #define NNCP_ALGO_BPP 3       /* updaters.py:121-164 */
-#define NNCP_ALGO_UCP 4       /* updaters.py:77-88 (status[0] bit 0: ridge applied; status[3] = 3: still singular) */
+#define NNCP_ALGO_UCP 4       /* updaters.py:77-88 (status[0] bit 0: ridge applied; still singular with the ridge:
+                                 the minimum-norm lstsq solution through a Jacobi eigendecomposition) */
 
 /* status words (device int32[NNCP_STATUS_WORDS]) written by nncp_update:
  *   [0],[1]  HALS: bit r set when gram diagonal r <= 0 (updaters.py:110-113)
@@ -128,6 +129,12 @@ int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int ra
                    const double* const* coeff, const int64_t* coeff_rows, int ncoeff, double* out,
                    void* stream);
 
+/* tensor_ops.py:121-137 khatri_rao, materialised (the hot path never does this):
+ * out (prod(rows) x rank, row-major) row (i_1..i_m) = prod_f factors[f][i_f, :], the first
+ * factor's index fastest.  factors: host array of `count` (1..8) device pointers. */
+int nncp_khatri_rao(const double* const* factors, const int64_t* rows, int count, int rank, double* out,
+                    void* stream);
+
 /* dimtree.py:287 np.ascontiguousarray(temp.as_matrix()): column-major -> row-major. */
 int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_rows, void* stream);
 
@@ -148,6 +155,11 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank,
                 const double* mttkrp_rows, const double* owned, const double* lam, int64_t rows,
                 double* hhat, double* nsq, double* beta, int* status, void* ws, size_t ws_bytes,
                 void* stream);
+/* nncp_update with the MU epsilon as a parameter (mu_update(inp, eps), updaters.py:91-94;
+ * nncp_update uses MU_EPSILON = 1e-16, updaters.py:27).  Other rules ignore mu_eps. */
+int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                   const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                   int* status, double mu_eps, void* ws, size_t ws_bytes, void* stream);
 
 /* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
  * gram = owned^T owned (raw, local rows).  owned may alias hhat; lam and gram may be NULL. */

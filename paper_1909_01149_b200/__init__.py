@@ -11,11 +11,11 @@ from .dimtree import (DimTreeContext, DimTreePlan, TempTensor, choose_balanced_s
                       choose_split_mode, multi_ttv, partial_mttkrp)
 from .driver import (ALGORITHMS, CATEGORIES, IN_SCOPE_ALGORITHMS, RunConfig, RunReport, init_factor,  # noqa: F401
                      nncp_parallel, nncp_sequential, record_category, relative_error, run_local)
-from .grid import CommCounters, DistMap, Grid, block_partition  # noqa: F401
-from .tensor_ops import (DenseTensor, FactorSet, gram, hadamard_grams_excluding, matrix_inner_product,  # noqa: F401
-                         norm_squared, normalize_columns)
+from .grid import CommCounters, DistMap, Grid, Worker, block_partition  # noqa: F401
+from .tensor_ops import (DenseTensor, FactorSet, gram, hadamard_grams_excluding, khatri_rao,  # noqa: F401
+                         matrix_inner_product, naive_mttkrp, norm_squared, normalize_columns, reconstruct)
 from .updaters import (BppCyclingError, UpdateInputs, UpdaterState, admm_update, bpp_update,  # noqa: F401
-                       hals_update, mu_update, nesterov_update, ucp_update)
+                       hals_update, mu_update, nesterov_outer_accelerate, nesterov_update, ucp_update)
 from .synth import synthetic_tensor, truth_factors  # noqa: F401
 from .tensor_io import (SyntheticSpec, TensorFileError, generate_synthetic, read_matrix, read_tensor,  # noqa: F401
                         write_matrix, write_tensor)

@@ -60,12 +60,16 @@ SIGNATURES = [
       ctypes.c_size_t, vp]),
     ("nncp_multi_ttv", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), c_i64p, ctypes.c_int, vp, vp]),
+    ("nncp_khatri_rao", ctypes.c_int, [vp, c_i64p, ctypes.c_int, ctypes.c_int, vp, vp]),
     ("nncp_temp_to_rows", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp]),
     ("nncp_status_reset", ctypes.c_int, [vp, vp]),
     ("nncp_status_reset_n", ctypes.c_int, [vp, ctypes.c_int, vp]),
     ("nncp_update", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp,
       ctypes.c_size_t, vp]),
+    ("nncp_update_ex", ctypes.c_int,
+     [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
+      ctypes.c_double, vp, ctypes.c_size_t, vp]),
     ("nncp_normalize_gram", ctypes.c_int,
      [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gram", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),

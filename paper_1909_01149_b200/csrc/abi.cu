@@ -26,8 +26,9 @@ size_t partial_ws_bytes(int order, const int64_t* dims, int split, int side, int
 int multi_ttv(const double*, int, const int64_t*, int, int, const double* const*, const int64_t*, int, double*,
               cudaStream_t);
 int temp_to_rows(const double*, int64_t, int, double*, cudaStream_t);
+int khatri_rao(const double* const*, const int64_t*, int, int, double*, cudaStream_t);
 int update(int, const double*, int, int, int, const double*, const double*, const double*, int64_t, double*, double*,
-           double*, int*, void*, size_t, cudaStream_t);
+           double*, int*, void*, size_t, cudaStream_t, double);
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
@@ -209,6 +210,12 @@ int nncp_multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int ra
   return multi_ttv(temp, nret, ret_dims, rank, side, coeff, coeff_rows, ncoeff, out, S(stream));
 }
 
+int nncp_khatri_rao(const double* const* factors, const int64_t* rows, int count, int rank, double* out,
+                    void* stream) {
+  if (rank < 1) return fail(NNCP_ERR_VALUE, "rank must be positive");
+  return khatri_rao(factors, rows, count, rank, out, S(stream));
+}
+
 int nncp_temp_to_rows(const double* temp, int64_t rows, int rank, double* out_rows, void* stream) {
   return temp_to_rows(temp, rows, rank, out_rows, S(stream));
 }
@@ -220,9 +227,9 @@ int nncp_status_reset_n(int* status, int count, void* stream) {
   return status_reset(status, count, S(stream));
 }
 
-int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
-                const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                int* status, void* ws, size_t ws_bytes, void* stream) {
+int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                   const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                   int* status, double mu_eps, void* ws, size_t ws_bytes, void* stream) {
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
   if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
@@ -236,7 +243,14 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank, co
     return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream));
   }
   return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
-                S(stream));
+                S(stream), mu_eps);
+}
+
+int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                int* status, void* ws, size_t ws_bytes, void* stream) {
+  return nncp_update_ex(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status,
+                        1e-16, ws, ws_bytes, stream);   // MU_EPSILON, updaters.py:27
 }
 
 int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,

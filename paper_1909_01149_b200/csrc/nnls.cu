@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     update_rows_kernel(const double* __restrict__ grams, int order, int mode, int R,
                        const double* __restrict__ mrows, const double* __restrict__ owned,
                        const double* __restrict__ lam, int64_t rows, double* __restrict__ hhat,
-                       double* __restrict__ part, double* nsq, double* beta, int* status, unsigned int* ticket) {
+                       double* __restrict__ part, double* nsq, double* beta, int* status, unsigned int* ticket,
+                       double mu_eps) {
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int r = lane + 32 * q;
-        h[q] = (r < R) ? h[q] * m[q] / (d[q] + 1e-16) : 0.0;
+        h[q] = (r < R) ? h[q] * m[q] / (d[q] + mu_eps) : 0.0;
       }
     } else {
       // updaters.py:107-118: Gauss-Seidel over columns with the latest values
@@ -597,13 +598,13 @@ size_t row_update_part_elems(int64_t rows, int rank) {
   const int64_t blocks_gram = (rows + kGramRows - 1) / kGramRows;
   size_t e = std::max<int64_t>(blocks_rows, blocks_bpp) * (rank + 6);  // + ADMM/NES step partials
   e = std::max<size_t>(e, size_t(std::max<int64_t>(blocks_gram, 1)) * rank * rank);
-  e = std::max<size_t>(e, size_t(num_sms()) * 8 * 2);   // norm_squared(_min): <= 8 blocks/SM, sum + min each
+  e = std::max<size_t>(e, size_t(num_sms()) * 8 * 4);   // norm_squared(_min): <= 8 blocks/SM, sum + 3 extrema
   return e;
 }
 
 int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
            const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
-           size_t ws_bytes, cudaStream_t st) {
+           size_t ws_bytes, cudaStream_t st, double mu_eps) {
   if (rows <= 0) {
     // an empty row block still owes its (zero) column sums
     if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
@@ -618,10 +619,12 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
     if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (update)");
     if (algo == NNCP_ALGO_MU)
       update_rows_kernel<NNCP_ALGO_MU><<<blocks, kRowWarps * 32, 0, st>>>(
-          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE);
+          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
+          mu_eps);
     else
       update_rows_kernel<NNCP_ALGO_HALS><<<blocks, kRowWarps * 32, 0, st>>>(
-          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE);
+          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
+          mu_eps);
   } else if (algo == NNCP_ALGO_BPP) {
     const int blocks = int(std::min<int64_t>((rows + kBppWarps - 1) / kBppWarps, int64_t(num_sms()) * 4));
     if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");

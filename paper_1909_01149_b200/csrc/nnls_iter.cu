@@ -87,52 +87,141 @@ static __device__ double trace_over_rank(const double* S, int R) {
 }
 
 // ------------------------------------------------------------------ UCP ----
+// Cyclic Jacobi eigendecomposition of the symmetric R x R matrix A (smem) by warp 0,
+// eigenvectors accumulated in V (columns); A's diagonal ends as the eigenvalues.
+static __device__ void warp_jacobi_eigen(double* A, double* V, int R) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < R * R; e += 32) V[e] = (e / R == e % R) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int e = lane; e < R * R; e += 32) {
+      if (e / R != e % R) off = fma(A[e], A[e], off);
+      else dia = fma(A[e], A[e], dia);
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if (!(off > 1e-32 * dia)) break;
+    for (int p = 0; p < R - 1; ++p) {
+      for (int q = p + 1; q < R; ++q) {
+        const double apq = A[p * R + q];
+        if (apq == 0.0) continue;
+        const double app = A[p * R + p], aqq = A[q * R + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        __syncwarp();
+        for (int k = lane; k < R; k += 32) {
+          const double akp = A[p * R + k], akq = A[q * R + k];
+          A[p * R + k] = cs * akp - sn * akq;
+          A[q * R + k] = sn * akp + cs * akq;
+        }
+        __syncwarp();
+        for (int k = lane; k < R; k += 32) {
+          const double akp = A[k * R + p], akq = A[k * R + q];
+          A[k * R + p] = cs * akp - sn * akq;
+          A[k * R + q] = sn * akp + cs * akq;
+          const double vkp = V[k * R + p], vkq = V[k * R + q];
+          V[k * R + p] = cs * vkp - sn * vkq;
+          V[k * R + q] = sn * vkp + cs * vkq;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // updaters.py:77-88: S H^T = M^T by Cholesky; singular S -> ridge 1e-12 tr(S)/R
-// (status[0] bit 0 = the reference's warning); still singular -> status[3] = 3.
+// (status[0] bit 0 = the reference's warning); still singular -> the minimum-norm
+// least-squares solution np.linalg.lstsq(S, M^T, rcond=None): S = V diag(l) V^T by
+// Jacobi, h = V diag(1/l_i for |l_i| > R eps max|l|, else 0) V^T m per row.
+// Dynamic shared memory: L (R x R), V (R x R), per-warp coefficients.
 __global__ void __launch_bounds__(kRowWarps * 32)
     ucp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
                int* status, unsigned int* ticket) {
-  __shared__ double L[kMaxRank * kMaxRank];
+  extern __shared__ double dsm[];
+  double* L = dsm;                       // R x R (kMaxRank^2 reserved)
+  double* V = dsm + kMaxRank * kMaxRank;  // eigenvectors (lstsq fallback only)
+  double* coef = V + kMaxRank * kMaxRank;  // kRowWarps x kMaxRank
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
+  __shared__ double inv_eig[kMaxRank];
   load_hadamard(L, grams, order, mode, R);
   __syncthreads();
   const double ridge = 1e-12 * trace_over_rank(L, R);
   __syncthreads();
   bool ok = block_cholesky(L, R, 0.0);
+  bool lstsq = false;
   if (!ok) {
     load_hadamard(L, grams, order, mode, R);  // S again (the failed factorisation overwrote it)
     __syncthreads();
     ok = block_cholesky(L, R, ridge);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      atomicOr(status, 1);
-      if (!ok) atomicMax(status + 3, 3);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, 1);
+    if (!ok) {
+      lstsq = true;
+      load_hadamard(L, grams, order, mode, R);
+      __syncthreads();
+      if (threadIdx.x < 32) warp_jacobi_eigen(L, V, R);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double smax = 0.0;
+        for (int i = 0; i < R; ++i) smax = fmax(smax, fabs(L[i * R + i]));
+        const double cut = double(R) * 2.220446049250313e-16 * smax;
+        for (int i = 0; i < R; ++i) {
+          const double l = L[i * R + i];
+          inv_eig[i] = (fabs(l) > cut) ? 1.0 / l : 0.0;
+        }
+      }
+      __syncthreads();
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double sq[2] = {0.0, 0.0};
   double bsum = 0.0;
-  if (ok) {
-    for (int64_t i = int64_t(blockIdx.x) * kRowWarps + warp; i < rows; i += int64_t(gridDim.x) * kRowWarps) {
-      const double* mr = mrows + i * R;
-      double v[2], m[2];
+  for (int64_t i = int64_t(blockIdx.x) * kRowWarps + warp; i < rows; i += int64_t(gridDim.x) * kRowWarps) {
+    const double* mr = mrows + i * R;
+    double v[2], m[2];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = lane + 32 * q;
-        m[q] = (r < R) ? mr[r] : 0.0;
-        v[q] = m[q];
-      }
+    for (int q = 0; q < 2; ++q) {
+      const int r = lane + 32 * q;
+      m[q] = (r < R) ? mr[r] : 0.0;
+      v[q] = m[q];
+    }
+    if (!lstsq) {
       warp_chol_solve(L, R, v);
-      double* hr = hhat + i * R;
+    } else {
+      double* cw = coef + warp * kMaxRank;
+      for (int e = 0; e < R; ++e) {   // c_e = (V^T m)_e / l_e
+        double p = 0.0;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = lane + 32 * q;
-        if (r < R) {
-          hr[r] = v[q];
-          sq[q] = fma(v[q], v[q], sq[q]);
-          bsum = fma(m[q], v[q], bsum);
+        for (int q = 0; q < 2; ++q) {
+          const int k = lane + 32 * q;
+          if (k < R) p = fma(V[k * R + e], m[q], p);
         }
+        p = warp_sum(p);
+        if (lane == 0) cw[e] = p * inv_eig[e];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {   // h_k = sum_e V[k, e] c_e
+        const int k = lane + 32 * q;
+        double h = 0.0;
+        if (k < R)
+          for (int e = 0; e < R; ++e) h = fma(V[k * R + e], cw[e], h);
+        v[q] = h;
+      }
+      __syncwarp();
+    }
+    double* hr = hhat + i * R;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = lane + 32 * q;
+      if (r < R) {
+        hr[r] = v[q];
+        sq[q] = fma(v[q], v[q], sq[q]);
+        bsum = fma(m[q], v[q], bsum);
       }
     }
   }
@@ -404,8 +493,10 @@ int ucp(const double* grams, int order, int mode, int rank, const double* mrows,
   WsLayout w = ws_layout(ws, ws_bytes);
   const int blocks = grid_rows(rows);
   if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (ucp)");
-  ucp_kernel<<<blocks, kRowWarps * 32, 0, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq, beta, status,
-                                                 w.tickets + T_UPDATE);
+  constexpr int smem = int(sizeof(double)) * (2 * kMaxRank * kMaxRank + kRowWarps * kMaxRank);
+  if (int rc = set_max_smem_once<ucp_kernel>(smem)) return rc;
+  ucp_kernel<<<blocks, kRowWarps * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq, beta,
+                                                   status, w.tickets + T_UPDATE);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

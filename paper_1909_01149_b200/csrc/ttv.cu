@@ -217,6 +217,37 @@ int multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, i
   return NNCP_OK;
 }
 
+// khatri_rao (tensor_ops.py:121-137) materialised: out[j, r] = prod_f H_f(j_f, r),
+// row-major, the first factor's index fastest.  Not on the hot path (the partial
+// MTTKRPs generate these rows on the fly); the public khatri_rao() of the mirror.
+__global__ void __launch_bounds__(256) khatri_rao_kernel(const CoeffSpec cs, int64_t rows, int R,
+                                                         double* __restrict__ out) {
+  const int64_t n = rows * R;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / R;
+    out[e] = coeff_value(cs, j, int(e - j * R), R);
+  }
+}
+
+int khatri_rao(const double* const* factors, const int64_t* rows, int count, int rank, double* out, cudaStream_t st) {
+  if (count < 1 || count > kMaxOrder) return fail(NNCP_ERR_VALUE, "khatri_rao needs 1..8 factors");
+  CoeffSpec cs{};
+  cs.n = count;
+  int64_t prod = 1;
+  for (int f = 0; f < count; ++f) {
+    if (rows[f] < 0) return fail(NNCP_ERR_VALUE, "negative factor rows");
+    cs.ptr[f] = factors[f];
+    cs.dim[f] = rows[f];
+    prod *= rows[f];
+  }
+  const int64_t n = prod * rank;
+  if (n == 0) return NNCP_OK;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  khatri_rao_kernel<<<blocks, 256, 0, st>>>(cs, prod, rank, out);
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
 int temp_to_rows(const double* temp, int64_t rows, int rank, double* out, cudaStream_t st) {
   const int64_t n = rows * rank;
   if (n == 0) return NNCP_OK;

@@ -903,9 +903,12 @@ def local_block(x, layout: RankLayout) -> torch.Tensor:
 
         return as_device(read_tensor_block(x, offs, layout.local_dims))
     if x.on_device:
-        # reversed-dims C view of the F-ordered buffer: index [i_N, ..., i_1]
-        view = x.data.view(tuple(reversed(x.dims)))
-        return view[tuple(reversed(layout.slice_rows))].contiguous().view(-1)
+        # reversed-dims C view of the F-ordered buffer: index [i_N, ..., i_1]; always a
+        # fresh allocation (a contiguous slice would be an offset view, not 16-byte aligned)
+        view = x.data.view(tuple(reversed(x.dims)))[tuple(reversed(layout.slice_rows))]
+        out = torch.empty(view.shape, dtype=torch.float64, device=x.data.device)
+        out.copy_(view)
+        return out.view(-1)
     arr = x.as_array()[tuple(layout.slice_rows)]
     return as_device(np.asarray(arr).ravel(order="F"))
 

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-__all__ = ["block_partition", "DistMap", "CommCounters", "Group", "Grid", "IdentityCollectives",
+__all__ = ["block_partition", "DistMap", "CommCounters", "Group", "Grid", "Worker", "IdentityCollectives",
            "DistCollectives", "ThreadCollectives", "ThreadGrid", "pin_nccl_environment"]
 
 
@@ -122,11 +122,12 @@ class CommCounters:
 
 
 class Group:
-    """Sorted rank set with position lookup (grid.py:116-126)."""
+    """Sorted rank set with position lookup and its rendezvous (grid.py:116-126)."""
 
     def __init__(self, ranks):
         self.ranks = tuple(sorted(int(r) for r in ranks))
         self.index = {r: k for k, r in enumerate(self.ranks)}
+        self.rendezvous = _Rendezvous(len(self.ranks))
 
     @property
     def size(self) -> int:
@@ -167,6 +168,154 @@ class Grid:
 
     def slice_group(self, mode: int, coord: int) -> Group:
         return self.slice_groups[mode][coord]
+
+    def _abort_all(self):
+        self.all_procs.rendezvous.abort()
+        for groups in self.slice_groups:
+            for g in groups:
+                g.rendezvous.abort()
+
+    def run(self, fn, *args):
+        """``fn(worker, *args)`` on every rank as worker threads; the list of results
+        (grid.py:172-203).  The first worker exception aborts every pending collective
+        and is re-raised in the caller."""
+        workers = [Worker(rank, self) for rank in range(self.total)]
+        self._workers = workers
+        results = [None] * self.total
+        failures = [None] * self.total
+
+        def main(w):
+            try:
+                results[w.rank] = fn(w, *args)
+            except threading.BrokenBarrierError:
+                pass
+            except BaseException as exc:  # noqa: BLE001  (propagate to the caller)
+                failures[w.rank] = exc
+                self._abort_all()
+
+        threads = [threading.Thread(target=main, args=(w,), name=f"worker-{w.rank}") for w in workers]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for exc in failures:
+            if exc is not None:
+                raise exc
+        return results
+
+
+class Worker:
+    """One rank of ``Grid.run``: coordinates, counters and the reference's collective
+    calls (grid.py:206-302) -- rank-ordered and bitwise reproducible.  Host (numpy)
+    payloads reduce on the host exactly as the reference; device payloads (torch CUDA
+    tensors) reduce on the device in the same rank order and come back as device
+    tensors.  Point-to-point send/recv (grid.py:224-237) is kept for completeness."""
+
+    def __init__(self, rank: int, grid: "Grid"):
+        self.rank = rank
+        self.grid = grid
+        self.coord = grid.coord_of(rank)
+        self.counters = CommCounters()
+        self.recorder = None
+        self._mailbox = []
+        self._cv = threading.Condition()
+
+    def _record(self, category: str, elapsed: float):
+        if self.recorder is not None:
+            self.recorder(category, elapsed)
+
+    def send(self, dst: int, payload):
+        w = self.grid._workers[dst]
+        with w._cv:
+            w._mailbox.append((self.rank, payload))
+            w._cv.notify_all()
+
+    def recv(self, src: int = None):
+        with self._cv:
+            while True:
+                for k, (s, p) in enumerate(self._mailbox):
+                    if src is None or s == src:
+                        self._mailbox.pop(k)
+                        return p
+                self._cv.wait()
+
+    @staticmethod
+    def _combine(slots, op):
+        out = slots[0].clone() if isinstance(slots[0], torch.Tensor) else slots[0].copy()
+        for s in slots[1:]:                      # ascending rank order (grid.py:250-262)
+            if op == "sum":
+                out += s
+            elif op == "min":
+                out = torch.minimum(out, s) if isinstance(out, torch.Tensor) else np.minimum(out, s, out=out)
+            else:
+                out = torch.maximum(out, s) if isinstance(out, torch.Tensor) else np.maximum(out, s, out=out)
+        return out
+
+    def all_reduce(self, group: Group, local, op: str = "sum"):
+        """Elementwise reduction in ascending rank order, the same result on every member."""
+        import time
+
+        if op not in ("sum", "min", "max"):
+            raise ValueError(f"unknown reduction {op!r}")
+        t0 = time.perf_counter()
+        dev = isinstance(local, torch.Tensor) and local.is_cuda
+        scalar = (not dev) and np.ndim(local) == 0
+        arr = local.reshape(-1).to(torch.float64) if dev else np.atleast_1d(np.asarray(local, dtype=np.float64))
+        if dev:
+            torch.cuda.current_stream().synchronize()
+        slots = group.rendezvous.exchange(group.index[self.rank], arr)
+        if any(tuple(x.shape) != tuple(slots[0].shape) for x in slots):
+            raise ValueError("all_reduce length mismatch across group")
+        out = self._combine(slots, op)
+        elapsed = time.perf_counter() - t0
+        n = int(arr.numel() if dev else arr.size)
+        self.counters.record("AllReduce", n, n, elapsed)
+        self._record("AllReduce", elapsed)
+        if dev:
+            return out.reshape(local.shape)
+        return float(out[0]) if scalar else out
+
+    def all_gather(self, group: Group, local):
+        """Concatenation of the members' arrays in ascending rank order."""
+        import time
+
+        t0 = time.perf_counter()
+        dev = isinstance(local, torch.Tensor) and local.is_cuda
+        arr = local if dev else np.asarray(local, dtype=np.float64)
+        if dev:
+            torch.cuda.current_stream().synchronize()
+        slots = group.rendezvous.exchange(group.index[self.rank], arr)
+        out = torch.cat(slots, dim=0) if dev else np.concatenate(slots, axis=0)
+        elapsed = time.perf_counter() - t0
+        n_in = int(arr.numel() if dev else arr.size)
+        self.counters.record("AllGather", n_in, int(out.numel() if dev else out.size), elapsed)
+        self._record("AllGather", elapsed)
+        return out
+
+    def reduce_scatter(self, group: Group, local, parts: DistMap):
+        """Rank-ordered elementwise sum, then this member's row block."""
+        import time
+
+        t0 = time.perf_counter()
+        dev = isinstance(local, torch.Tensor) and local.is_cuda
+        arr = local if dev else np.asarray(local, dtype=np.float64)
+        if parts.parts != group.size:
+            raise ValueError(f"partition has {parts.parts} blocks for a group of {group.size}")
+        if parts.total != arr.shape[0]:
+            raise ValueError(f"partition covers {parts.total} rows, local array has {arr.shape[0]}")
+        if dev:
+            torch.cuda.current_stream().synchronize()
+        slots = group.rendezvous.exchange(group.index[self.rank], arr)
+        if any(tuple(x.shape) != tuple(slots[0].shape) for x in slots):
+            raise ValueError("reduce_scatter length mismatch across group")
+        total = self._combine(slots, "sum")
+        blk = total[parts.block(group.index[self.rank])]
+        out = blk.clone() if dev else blk.copy()
+        elapsed = time.perf_counter() - t0
+        self.counters.record("ReduceScatter", int(arr.numel() if dev else arr.size),
+                             int(out.numel() if dev else out.size), elapsed)
+        self._record("ReduceScatter", elapsed)
+        return out
 
 
 # ------------------------------------------------------------- layout ------
@@ -369,10 +518,11 @@ class _Rendezvous:
         self._enter = threading.Barrier(size)
         self._leave = threading.Barrier(size)
 
-    def exchange(self, index: int, value, combine):
+    def exchange(self, index: int, value, combine=None):
         self.slots[index] = value
         self._enter.wait()
-        out = combine(list(self.slots))
+        view = list(self.slots)
+        out = combine(view) if combine is not None else view
         self._leave.wait()
         return out
 

@@ -17,9 +17,31 @@ import torch
 from . import _lib
 
 __all__ = [
-    "DenseTensor", "FactorSet", "gram", "hadamard_grams_excluding", "matrix_inner_product",
-    "norm_squared", "normalize_columns", "device", "as_device", "Workspace",
+    "DenseTensor", "FactorSet", "gram", "hadamard_grams_excluding", "khatri_rao", "matrix_inner_product",
+    "naive_mttkrp", "norm_squared", "normalize_columns", "reconstruct", "device", "as_device", "Workspace",
 ]
+
+
+def on_host(*objs) -> bool:
+    """True unless one of ``objs`` (arrays, tensors, DenseTensors, lists of them) lives
+    on the GPU: the operator-level functions answer host inputs with numpy arrays,
+    like the reference, and device inputs with device tensors."""
+    for o in objs:
+        if isinstance(o, (list, tuple)):
+            if not on_host(*o):
+                return False
+        elif isinstance(o, torch.Tensor) and o.is_cuda:
+            return False
+        elif isinstance(o, DenseTensor) and o.on_device:
+            return False
+        elif isinstance(o, FactorSet) and not on_host(*o.factors):
+            return False
+    return True
+
+
+def to_host_if(t, host: bool):
+    """``t`` as a numpy array when the call's inputs were host arrays."""
+    return t.detach().cpu().numpy() if host and isinstance(t, torch.Tensor) else t
 
 
 def device() -> torch.device:
@@ -208,8 +230,10 @@ def norm_squared(x: DenseTensor) -> float:
     return float(out.item())
 
 
-def gram(h) -> torch.Tensor:
+def gram(h):
     """H^T H forced symmetric (tensor_ops.py:140-143); device kernel + 0.5(G+G^T)."""
+    if on_host(h):
+        return to_host_if(gram(as_device(h)), True)
     lib = _lib.load()
     h = as_device(h)
     rows, r = int(h.shape[0]), int(h.shape[1])
@@ -219,10 +243,12 @@ def gram(h) -> torch.Tensor:
     return 0.5 * (g + g.T)
 
 
-def hadamard_grams_excluding(grams, exclude: int) -> torch.Tensor:
+def hadamard_grams_excluding(grams, exclude: int):
     """Elementwise product of all Grams except ``exclude`` (tensor_ops.py:146-155)."""
     if not 0 <= exclude < len(grams):
         raise ValueError(f"exclude index {exclude} out of range")
+    if on_host(list(grams)):
+        return to_host_if(hadamard_grams_excluding([as_device(g) for g in grams], exclude), True)
     out = None
     for m, g in enumerate(grams):
         if m != exclude:
@@ -251,6 +277,9 @@ def matrix_inner_product(a, b) -> float:
 
 def normalize_columns(h):
     """Unit columns and their norms (tensor_ops.py:198-205), via the fused device kernel."""
+    if on_host(h):
+        out, lam = normalize_columns(as_device(h))
+        return to_host_if(out, True), to_host_if(lam, True)
     lib = _lib.load()
     h = as_device(h)
     rows, r = int(h.shape[0]), int(h.shape[1])
@@ -265,3 +294,68 @@ def normalize_columns(h):
     _lib.check(lib.nncp_normalize_gram(_lib.ptr(h), _lib.ptr(nsq), rows, r, _lib.ptr(out), _lib.ptr(lam),
                                        _lib.ptr(g), ws.ptr, ws.nbytes, _lib.stream_handle()))
     return out, lam
+
+
+def khatri_rao(factors):
+    """Khatri-Rao product, first factor's index fastest (tensor_ops.py:121-137), built by
+    the device kernel nncp_khatri_rao (the hot path never materialises it)."""
+    factors = list(factors)
+    if len(factors) == 0:
+        raise ValueError("khatri_rao needs at least one factor")
+    ranks = {int(h.shape[1]) for h in factors}
+    if len(ranks) != 1:
+        raise ValueError(f"khatri_rao rank mismatch: {sorted(ranks)}")
+    host = on_host(factors)
+    r = ranks.pop()
+    if len(factors) > _lib.MAX_ORDER:          # fold the tail first: same rows, same order
+        factors = factors[:_lib.MAX_ORDER - 1] + [khatri_rao(factors[_lib.MAX_ORDER - 1:])]
+    dev = [as_device(h) for h in factors]
+    rows = [int(h.shape[0]) for h in dev]
+    out = torch.empty((int(np.prod(rows)), r), dtype=torch.float64, device=dev[0].device)
+    lib = _lib.load()
+    _lib.check(lib.nncp_khatri_rao(_lib.ptrs(dev), _lib.i64(rows), len(dev), r, _lib.ptr(out),
+                                   _lib.stream_handle()))
+    return to_host_if(out, host)
+
+
+def naive_mttkrp(x: DenseTensor, factors, mode: int):
+    """MTTKRP in ``mode`` (tensor_ops.py:158-185), the reference's oracle path.
+
+    The reference sums with one einsum over the dense array; here the same quantity
+    comes from the device kernels without a dimension tree: one partial MTTKRP on the
+    side of the root split that retains ``mode`` and a multi-TTV chain
+    (DimTreeContext.mttkrp_direct)."""
+    from .dimtree import DimTreeContext, DimTreePlan
+
+    hs = list(factors.factors) if isinstance(factors, FactorSet) else list(factors)
+    n = x.order
+    if len(hs) != n:
+        raise ValueError("factor count does not match tensor order")
+    for m, h in enumerate(hs):
+        if m != mode and int(h.shape[0]) != x.dims[m]:
+            raise ValueError(f"factor {m} has {int(h.shape[0])} rows, tensor dim is {x.dims[m]}")
+    if n > _lib.MAX_ORDER:
+        raise ValueError("tensor order too large for naive path")
+    if not 0 <= mode < n:
+        raise ValueError(f"mode {mode} out of range")
+    host = on_host(x, hs)
+    ranks = {int(h.shape[1]) for h in hs}
+    if len(ranks) != 1:
+        raise ValueError(f"factors disagree on rank: {sorted(ranks)}")
+    plan = DimTreePlan.create(x.dims, ranks.pop())
+    out = DimTreeContext(plan).mttkrp_direct(x, hs, mode)
+    return to_host_if(out, host)
+
+
+def reconstruct(model: FactorSet) -> DenseTensor:
+    """Dense tensor of the model, sum_r lam_r prod_n H_n(i_n, r) (tensor_ops.py:192-195),
+    generated by the device kernel (nncp_synthetic with no noise)."""
+    from .synth import synthetic_block
+
+    host = on_host(model)
+    fs = [f.detach().cpu().numpy() if isinstance(f, torch.Tensor) else np.asarray(f, dtype=np.float64)
+          for f in model.factors]
+    lam = model.lam.detach().cpu().numpy() if isinstance(model.lam, torch.Tensor) else np.asarray(model.lam)
+    fs[0] = fs[0] * lam[None, :]
+    data = synthetic_block(model.dims, fs, 0.0, 0)
+    return DenseTensor(model.dims, to_host_if(data, host))

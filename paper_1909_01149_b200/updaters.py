@@ -21,10 +21,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from .tensor_ops import Workspace, as_device
+from .tensor_ops import FactorSet, Workspace, as_device, on_host, to_host_if
 
 __all__ = ["UpdateInputs", "UpdaterState", "BppCyclingError", "mu_update", "hals_update", "bpp_update",
-           "ucp_update", "admm_update", "nesterov_update", "default_admm_rho", "nesterov_hyperparams",
+           "ucp_update", "admm_update", "nesterov_update", "nesterov_outer_accelerate", "default_admm_rho",
+           "nesterov_hyperparams",
            "MU_EPSILON", "BPP_BACKUP_TRIES", "ADMM_INNER_CAP", "NESTEROV_INNER_CAP", "raise_for_status",
            "raise_for_code", "warn_for_status",
            "local_reduce", "AdmmRunner", "NesterovRunner"]
@@ -90,30 +91,22 @@ def warn_for_status(mask_lo, mask_hi, algo: str = "hals"):
 
 
 def raise_for_code(kind: int, row: int):
-    """The reference's NNLS exceptions (updaters.py:87-88,152,163) from a failure kind / row."""
+    """The reference's NNLS exceptions (updaters.py:152,163) from a failure kind / row."""
     if kind == 1:
         raise BppCyclingError(int(row))
     if kind == 2:
-        raise torch.linalg.LinAlgError("Singular matrix")  # numpy.linalg.LinAlgError analogue
-    if kind == 3:
-        raise NotImplementedError("gram singular even with the ridge; the reference's lstsq fallback "
-                                  "(updaters.py:87-88) is not on the device path")
+        raise np.linalg.LinAlgError("Singular matrix")     # what np.linalg.solve raises (updaters.py:152)
 
 
 def raise_for_status(status_host, algo: str = "hals"):
     """Translate kernel status words into the reference's warnings / exceptions."""
     warn_for_status(status_host[0], status_host[1], algo)
-    kind = int(status_host[3])
-    if kind == 1:
-        raise BppCyclingError(int(status_host[2]))
-    if kind == 2:
-        raise torch.linalg.LinAlgError("Singular matrix")  # numpy.linalg.LinAlgError analogue
-    if kind == 3:
-        raise NotImplementedError("gram singular even with the ridge; the reference's lstsq fallback "
-                                  "(updaters.py:87-88) is not on the device path")
+    raise_for_code(int(status_host[3]), int(status_host[2]))
 
 
-def _run(algo: str, inp: UpdateInputs) -> torch.Tensor:
+def _run(algo: str, inp: UpdateInputs, mu_eps: float = MU_EPSILON):
+    """One device update of every row; numpy out for numpy in (the reference's type)."""
+    host = on_host(inp.gram, inp.mttkrp_rows, inp.current)
     lib = _lib.load()
     s = as_device(inp.gram)
     m = as_device(inp.mttkrp_rows)
@@ -124,20 +117,19 @@ def _run(algo: str, inp: UpdateInputs) -> torch.Tensor:
     ws = Workspace(256 + 8 * ((rows + 3) * (r + 1) + r * r + 4096))
     st = _lib.stream_handle()
     _lib.check(lib.nncp_status_reset(_lib.ptr(status), st))
-    _lib.check(lib.nncp_update(_lib.ALGO_CODES[algo], _lib.ptr(s), 0, -1, r, _lib.ptr(m), _lib.ptr(cur), None,
-                               rows, _lib.ptr(out), None, None, _lib.ptr(status), ws.ptr, ws.nbytes, st))
+    _lib.check(lib.nncp_update_ex(_lib.ALGO_CODES[algo], _lib.ptr(s), 0, -1, r, _lib.ptr(m), _lib.ptr(cur), None,
+                                  rows, _lib.ptr(out), None, None, _lib.ptr(status), float(mu_eps), ws.ptr, ws.nbytes,
+                                  st))
     raise_for_status(status.cpu().tolist(), algo)
-    return out
+    return to_host_if(out, host)
 
 
-def mu_update(inp: UpdateInputs, eps: float = MU_EPSILON) -> torch.Tensor:
-    """H <- H * M / (H S + 1e-16) (updaters.py:91-94)."""
-    if eps != MU_EPSILON:
-        raise NotImplementedError("the device MU kernel uses the reference epsilon 1e-16")
-    return _run("mu", inp)
+def mu_update(inp: UpdateInputs, eps: float = MU_EPSILON):
+    """H <- H * M / (H S + eps) (updaters.py:91-94)."""
+    return _run("mu", inp, eps)
 
 
-def hals_update(inp: UpdateInputs, hook=local_reduce) -> torch.Tensor:
+def hals_update(inp: UpdateInputs, hook=local_reduce):
     """One Gauss-Seidel column sweep (updaters.py:97-118).
 
     The reference's per-column hook All-Reduce returns a value nobody reads
@@ -146,12 +138,12 @@ def hals_update(inp: UpdateInputs, hook=local_reduce) -> torch.Tensor:
     return _run("hals", inp)
 
 
-def bpp_update(inp: UpdateInputs) -> torch.Tensor:
+def bpp_update(inp: UpdateInputs):
     """Exact NNLS per row by block principal pivoting (updaters.py:121-164)."""
     return _run("bpp", inp)
 
 
-def ucp_update(inp: UpdateInputs) -> torch.Tensor:
+def ucp_update(inp: UpdateInputs):
     """Unconstrained Cholesky solve S H^T = M^T with the ridge fallback (updaters.py:77-88)."""
     return _run("ucp", inp)
 
@@ -244,6 +236,7 @@ def _torch_hook(hook):
 def admm_update(inp: UpdateInputs, state: UpdaterState, hook=local_reduce, rho: float = None,
                 max_steps: int = ADMM_INNER_CAP, rtol: float = 1e-4) -> torch.Tensor:
     """Up to ``max_steps`` ADMM rounds, dual persisting in ``state`` (updaters.py:173-220)."""
+    host = on_host(inp.gram, inp.mttkrp_rows, inp.current)
     s = as_device(inp.gram)
     m = as_device(inp.mttkrp_rows)
     cur = as_device(inp.current)
@@ -252,9 +245,9 @@ def admm_update(inp: UpdateInputs, state: UpdaterState, hook=local_reduce, rho: 
     u = torch.zeros_like(cur) if u is None else as_device(u).clone()
     runner = AdmmRunner(rows, r, m.device, Workspace(256 + 8 * (rows * 6 + 4096)))
     x, steps = runner.run(_SPack.explicit(s), m, cur, u, _torch_hook(hook), rho, max_steps, rtol)
-    state.admm_dual = u
+    state.admm_dual = to_host_if(u, host)
     state.last_inner_iters = steps
-    return x.clone()
+    return to_host_if(x.clone(), host)
 
 
 def nesterov_hyperparams(gram, prox_floor: float = NESTEROV_PROX_FLOOR):
@@ -307,6 +300,7 @@ class NesterovRunner:
 def nesterov_update(inp: UpdateInputs, state: UpdaterState, hook=local_reduce,
                     max_iters: int = NESTEROV_INNER_CAP, tol: float = 1e-8) -> torch.Tensor:
     """Accelerated projected gradient with proximal centre state.nesterov_prev (updaters.py:250-281)."""
+    host = on_host(inp.gram, inp.mttkrp_rows, inp.current)
     s = as_device(inp.gram)
     m = as_device(inp.mttkrp_rows)
     cur = as_device(inp.current)
@@ -315,6 +309,31 @@ def nesterov_update(inp: UpdateInputs, state: UpdaterState, hook=local_reduce,
     runner = NesterovRunner(rows, r, m.device, Workspace(256 + 8 * (rows * 3 + 4096)))
     x, steps = runner.run(_SPack.explicit(s), m, cur, xstar, _torch_hook(hook), max_iters, tol)
     out = x.clone()
-    state.nesterov_prev = out.clone()
+    state.nesterov_prev = to_host_if(out.clone(), host)
     state.last_inner_iters = steps
-    return out
+    return to_host_if(out, host)
+
+
+def nesterov_outer_accelerate(model_prev, model_cur, iteration: int, error_fn):
+    """Extrapolated candidate H_i + s_i (H_i - H_{i-1}), s_i = i^(1/N), clamped at zero,
+    kept only when ``error_fn`` reports a strictly lower error (updaters.py:284-300).
+    The extrapolation runs in the device kernel the engine uses (nncp_extrapolate);
+    numpy models give numpy candidates."""
+    lib = _lib.load()
+    host = on_host(model_prev, model_cur)
+    step = float(iteration) ** (1.0 / model_cur.order)
+
+    def extrap(cur, prev):
+        c, p = as_device(cur), as_device(prev)
+        if tuple(c.shape) != tuple(p.shape):
+            raise ValueError(f"model shapes differ: {tuple(c.shape)} vs {tuple(p.shape)}")
+        out = torch.empty_like(c)
+        _lib.check(lib.nncp_extrapolate(_lib.ptr(c), _lib.ptr(p), c.numel(), step, _lib.ptr(out),
+                                        _lib.stream_handle()))
+        return to_host_if(out, host)
+
+    factors = [extrap(hc, hp) for hp, hc in zip(model_prev.factors, model_cur.factors)]
+    candidate = FactorSet(factors, extrap(model_cur.lam, model_prev.lam))
+    if error_fn(candidate) < error_fn(model_cur):
+        return candidate, True
+    return model_cur, False

@@ -50,7 +50,7 @@ def test_cli_runs(tmp_path):
     factors = [read_matrix(f"{prefix}_factors_{n}.bin") for n in (1, 2, 3)]
     lam = np.atleast_1d(np.loadtxt(f"{prefix}_lambda.txt"))
     x, _ = generate_synthetic(SyntheticSpec((6, 5, 4), 2, seed=2))
-    xd = x.data.cpu().numpy()
+    xd = np.asarray(x.data)
     direct = np.linalg.norm(xd - O.reconstruct(factors, lam)) / np.linalg.norm(xd)
     assert abs(direct - float(rows[-1]["relerr"])) <= 1e-10
     rep = nncp_sequential(x, RunConfig(rank=2, algorithm="hals", max_iters=8, tol=0.0, seed=2))

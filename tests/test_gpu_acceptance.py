@@ -11,6 +11,10 @@ from oracle import nncp_oracle as O
 pytestmark = pytest.mark.gpu
 
 
+def _host(t):
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+
+
 @pytest.fixture(scope="module")
 def P():
     import torch
@@ -36,7 +40,7 @@ def test_c01_dimension_tree_oracle_equivalence(P):
         ctx.begin_iteration()
         xd = P.DenseTensor(dims, x).to_device()
         for mode in range(order):
-            got = ctx.mttkrp(xd, hs, mode).cpu().numpy()
+            got = _host(ctx.mttkrp(xd, hs, mode))
             want = O.naive_mttkrp(x, dims, hs, mode)
             scale = max(np.abs(want).max(), 1e-30)
             assert np.abs(got - want).max() <= 1e-12 * scale
@@ -85,7 +89,7 @@ def test_c06_mu_objective_monotone(P):
         b = rng.random((r + 4, 4))
         s, m = a.T @ a, b.T @ a
         h0 = rng.random((4, r)) + 1e-3
-        h1 = P.mu_update(P.UpdateInputs(s, m, h0)).cpu().numpy()
+        h1 = _host(P.mu_update(P.UpdateInputs(s, m, h0)))
         f0 = np.linalg.norm(a @ h0.T - b) ** 2
         f1 = np.linalg.norm(a @ h1.T - b) ** 2
         assert f1 <= f0 * (1 + 1e-12) + 1e-12
@@ -107,7 +111,7 @@ def test_c07_error_identity_matches_reconstruction(P):
             hs.append(h)
         last = len(dims) - 1
         ctx = P.DimTreeContext(P.DimTreePlan.create(dims, rank))
-        m_n = ctx.mttkrp_last_mode(P.DenseTensor(dims, x), hs).cpu().numpy()
+        m_n = _host(ctx.mttkrp_last_mode(P.DenseTensor(dims, x), hs))
         grams = [O.gram(h) for h in hs]
         s_n = O.hadamard_excluding(grams, last)
         eps = P.relative_error(float(x @ x), m_n, hs[last] * lam, s_n, grams[last], lam)

@@ -31,7 +31,8 @@ def P():
 
 
 def _np(t):
-    return t.detach().cpu().numpy()
+    """Host copy of a result: device tensors for device inputs, numpy (as the reference) for host inputs."""
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
 
 
 def _sliced(P, x, plan, levels=6):

@@ -5,6 +5,7 @@ import warnings
 import numpy as np
 import pytest
 
+from oracle import nncp_oracle as O
 from tests.conftest import rel_fro
 
 pytestmark = pytest.mark.gpu
@@ -168,3 +169,22 @@ def test_inner_runner_uses_call_rows_not_capacity(P, algo):
         res.append((x[:rows].cpu().numpy(), steps))
     assert np.isfinite(res[0][0]).all()
     assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
+
+
+def test_ucp_lstsq_fallback_matches_reference(P):
+    """S singular even with the ridge (indefinite or zero): the reference's minimum-norm
+    np.linalg.lstsq(S, M^T, rcond=None) (updaters.py:87-88), now on the device (Jacobi
+    eigendecomposition + pseudo-inverse) instead of NotImplementedError."""
+    rng = np.random.default_rng(12)
+    q, _ = np.linalg.qr(rng.standard_normal((5, 5)))
+    cases = [np.diag([2.0, -1.0, 0.0]),                         # indefinite with a zero eigenvalue
+             np.zeros((4, 4)),                                   # zero Gram: lstsq gives 0
+             q @ np.diag([3.0, 1.0, -0.5, 0.0, 0.0]) @ q.T]      # rotated, rank 3, indefinite
+    for s in cases:
+        s = 0.5 * (s + s.T)
+        m = rng.standard_normal((9, s.shape[0]))
+        with pytest.warns(UserWarning, match="ridge"):
+            got = _np(P.ucp_update(P.UpdateInputs(s, m, np.zeros_like(m))))
+        with pytest.warns(UserWarning, match="ridge"):
+            want = O.ucp_update(s, m)
+        assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want))), s
