@@ -209,11 +209,11 @@ class _EventTimer:
         self._marks, self._start = [], None
         self.capturing = False
 
-    def collect_graph(self, row: dict):
-        """Per-category seconds of the last graph replay (after the stream is synchronised)."""
-        if not self.enabled or self.graph_marks is None:
+    def collect_marks(self, graph_marks, row: dict):
+        """Per-category seconds of a finished graph replay whose marks are ``graph_marks``."""
+        if not self.enabled or graph_marks is None:
             return
-        prev, marks = self.graph_marks
+        prev, marks = graph_marks
         for cat, tag, e in marks:
             dt = prev.elapsed_time(e) / 1e3
             row[cat] += dt
@@ -491,7 +491,7 @@ class _Engine:
             else:
                 self.runner = NesterovRunner(rows_max, R, dev, self.ws)
                 self.nes_prev = [None] * N
-        self.graph = None
+        self.graphs = []            # [(CUDA graph of one sweep, its timing marks)]
         # capture stream created up front: torch's first Stream() builds its stream pool
         # (~14 ms, measured), which here overlaps an asynchronous tensor upload
         self.capture_stream = torch.cuda.Stream() if cfg.cuda_graph is not False else None
@@ -502,6 +502,12 @@ class _Engine:
     # -- small wrappers -------------------------------------------------------
     def _st(self):
         return _lib.stream_handle()
+
+    def _cmark(self, category):
+        """Timer mark after a collective; a single context's collectives are no-ops, and
+        an event-record node costs ~1-2 us of GPU timeline, so none is recorded for them."""
+        if self.coll.parallel:
+            self.timer.mark(category)
 
     def _gather(self, n):
         if self.coll.parallel:
@@ -514,7 +520,7 @@ class _Engine:
         wall0 = self._wall0          # the norm pass ran in __init__ (it picks the engine)
         alpha_t = self.scal[2:3]
         self.coll.all_reduce(alpha_t)
-        self.timer.mark("AllReduce")
+        self._cmark("AllReduce")
         self.alpha = float(alpha_t.item())
         if self.warn_negative and self.facts.signed:
             warnings.warn("tensor has negative entries; nonnegative model will not fit")
@@ -542,9 +548,9 @@ class _Engine:
                                      self.ws.ptr, self.ws.nbytes, st))
             self.timer.mark("Gram")
             self.coll.all_reduce(self.grams[n])
-            self.timer.mark("AllReduce")
+            self._cmark("AllReduce")
             self._gather(n)
-            self.timer.mark("AllGather")
+            self._cmark("AllGather")
         self.report.split_mode = self.plan.split if cfg.use_dimtree else None
         # initial model error from an out-of-band last-mode MTTKRP (driver.py:362-373);
         # the reference uses the einsum oracle here, the device reuses the tree kernels
@@ -557,7 +563,7 @@ class _Engine:
                                   _lib.vp(self.scal.data_ptr() + 24), self.ws.ptr, self.ws.nbytes, st))
         self.timer.mark("Error")
         self.coll.all_reduce(self.scal[3:4])
-        self.timer.mark("AllReduce")
+        self._cmark("AllReduce")
         _lib.check(lib.nncp_gamma(_lib.ptr(self.grams), self.N, R, _lib.ptr(self.lam),
                                   _lib.vp(self.scal.data_ptr() + 8), st))
         self.timer.mark("Error")
@@ -581,7 +587,7 @@ class _Engine:
                 self.ctx.mttkrp_direct(self.x, self.shared, n, out=mb)
             self.timer.mark("MTTKRP")
             m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
-            self.timer.mark("ReduceScatter")
+            self._cmark("ReduceScatter")
             last = n == N - 1
             if cfg.algorithm in FUSED_ALGORITHMS:
                 _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
@@ -601,29 +607,29 @@ class _Engine:
                                          self.ws.ptr, self.ws.nbytes, st))
                 self.timer.mark("Gram")
                 self.coll.all_reduce(self.graw)
-                self.timer.mark("AllReduce")
+                self._cmark("AllReduce")
                 _lib.check(lib.nncp_normalize_from_gram(_lib.ptr(self.hhat), _lib.ptr(self.graw), self.n_owned[n],
                                                         R, _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
                                                         _lib.ptr(self.grams[n]), st))
                 self.timer.mark("NNLS")
             else:
                 self.coll.all_reduce(self.nsq)
-                self.timer.mark("AllReduce")
+                self._cmark("AllReduce")
                 _lib.check(lib.nncp_normalize_gram(_lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R,
                                                    _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
                                                    _lib.ptr(self.grams[n]), self.ws.ptr, self.ws.nbytes, st))
                 self.timer.mark("Gram")
                 self.coll.all_reduce(self.grams[n])
-                self.timer.mark("AllReduce")
+                self._cmark("AllReduce")
             self._gather(n)
-            self.timer.mark("AllGather")
+            self._cmark("AllGather")
         _lib.check(lib.nncp_gamma_publish(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam),
                                           _lib.vp(self.scal.data_ptr() + 8), _lib.ptr(self.status), N,
                                           _lib.vp(self.xvec.data_ptr() + 8), self.nranks * N, self.me * N,
                                           _lib.ptr(self.masks), st))
         self.timer.mark("Error")
         self.coll.all_reduce(self.xvec, words=1)      # beta + every rank's status codes
-        self.timer.mark("AllReduce")
+        self._cmark("AllReduce")
         self.host_xvec.copy_(self.xvec, non_blocking=True)
         self.host_scal.copy_(self.scal[0:2], non_blocking=True)
         self.host_masks.copy_(self.masks, non_blocking=True)
@@ -745,27 +751,29 @@ class _Engine:
         use_graph = (capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))) and self.fault is None
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
+        pending = None      # (marks, row) of the previous graph replay, read while the next one runs
         for it in range(done + 1, stop + 1):
             self.report.begin_row()
             wall0 = time.perf_counter()
-            if use_graph and self.graph is None and it > 1 and not self.graph_failed:
-                self._capture()
-            if self.graph is not None:
-                self.graph.replay()
-                if self.graph_replays:
-                    self.coll.counters.add(self.graph_comm)
+            if use_graph and not self.graphs and it > 1 and not self.graph_failed:
+                self._capture_graphs()
+            if self.graphs:
+                g, marks = self.graphs[self.graph_replays % len(self.graphs)]
+                g.replay()
+                self.coll.counters.add(self.graph_comm)
                 self.graph_replays += 1
                 if cfg.use_dimtree:
                     self.ctx.partial_calls += 2
+                if pending is not None:          # the GPU is busy with this replay meanwhile
+                    self.timer.collect_marks(*pending)
+                pending = (marks, self.report.rows[-1])
             else:
                 self.timer.start()
                 if cfg.algorithm == "nes":
                     self._snapshot()
                 self._sweep()
             eps = self._finish_iteration(it)
-            if self.graph is not None:
-                self.timer.collect_graph(self.report.rows[-1])
-            else:
+            if not self.graphs:
                 self.timer.collect(self.report.rows[-1])
             errors.append(eps)
             if cfg.algorithm == "nes":
@@ -775,10 +783,33 @@ class _Engine:
             if eps <= cfg.tol:
                 self.report.converged = True
                 break
+        if pending is not None:
+            self.timer.collect_marks(*pending)
         self.report.tree_partial_calls = self.ctx.partial_calls if cfg.use_dimtree else 0
 
+    @property
+    def graph(self):
+        return self.graphs[0][0] if self.graphs else None
+
+    def _capture_graphs(self):
+        """Two copies of the sweep graph with their own timing events, replayed alternately:
+        the host reads one replay's category events while the GPU runs the next, so the
+        per-iteration gap between replays is only the eps read-back (one graph when the
+        timing events are off)."""
+        first = self._capture()
+        if first is None:
+            return
+        graphs = [first]
+        if self.timer.enabled:
+            second = self._capture()
+            if second is None:
+                return
+            graphs.append(second)
+        self.graphs = graphs
+
     def _capture(self):
-        """Record one sweep as a CUDA graph (all buffers already allocated by sweep 1)."""
+        """Record one sweep as a CUDA graph (all buffers already allocated by sweep 1);
+        returns (graph, timing marks) or None when capture failed (eager from then on)."""
         calls = self.ctx.partial_calls
         launches0 = self.lib.nncp_launch_count()
         comm0 = self.coll.counters.snapshot()
@@ -805,14 +836,16 @@ class _Engine:
             self.ctx.partial_calls = calls
             self.coll.counters.restore(comm0)
             self.graph_failed = True
-            return
+            self.graphs = []
+            return None
         torch.cuda.current_stream().wait_stream(side)
         self.ctx.partial_calls = calls
         self.graph_kernels = int(self.lib.nncp_launch_count() - launches0)
-        # the collectives recorded once while capturing belong to the first replay;
-        # later replays add the same calls and words (grid.py:60-93 tallies per call)
+        # capturing ran no collective: every replay adds the captured calls and words
+        # (grid.py:60-93 tallies per call)
         self.graph_comm = self.coll.counters.since(comm0)
-        self.graph = g
+        self.coll.counters.restore(comm0)
+        return g, self.timer.graph_marks
 
     def model_host(self):
         return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()
