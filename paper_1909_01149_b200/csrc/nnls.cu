@@ -94,35 +94,432 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 }
 
 // ------------------------------------------------------------------ BPP ----
-// One warp per row: block principal pivoting (updaters.py:121-155) with the
-// passive-set solve done by warp-parallel LU with partial pivoting (dgesv).
-constexpr int kBppWarps = 4;
+// One warp per row: block principal pivoting (updaters.py:121-155).
+constexpr int kBppWarps = 4;   // warps per CTA at R > 48 (shared-memory bound)
+// Warps per CTA: the block-level S^-1 is a 2R-step Gauss-Jordan chain -- latency-bound,
+// so it wants many warps; every warp then solves its own rows.  The per-warp LU scratch
+// (R x (R+1) doubles) caps the count at large R.
+template <int RP>
+constexpr int bpp_warps() { return RP <= 32 ? 16 : (RP <= 48 ? 8 : kBppWarps); }
+
+// Warp LU with partial pivoting (first-max pivot, like dgesv) of the m x m system in A
+// (pitch LP, right-hand side in column m); the solution overwrites column m.  False
+// when a pivot is exactly zero (what makes np.linalg.solve raise LinAlgError).
+template <int RP>
+__device__ bool warp_lu_solve(double* A, int m, int LP) {
+  constexpr int NH = (RP + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  for (int cidx = 0; cidx < m; ++cidx) {
+    // pivot: max |A[i][c]| over i >= c, first index on ties (idamax).  Exact warp
+    // argmax in three reductions: |v| >= 0 orders like its bit pattern, so max of the
+    // high words, then of the low words among those, then the smallest row index
+    // among the exact maxima.
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int a = cidx + lane; a < m; a += 32) {
+      const double v = fabs(A[a * LP + cidx]);
+      if (v > bv) {
+        bv = v;
+        bi = a;
+      }
+    }
+    {
+      const bool cand = bi != INT_MAX;
+      const unsigned long long bits = cand ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, uint32_t(bits >> 32));
+      const unsigned tie = __ballot_sync(0xffffffffu, cand && uint32_t(bits >> 32) == mh);
+      if (__popc(tie) == 1) {   // one lane holds the high-word maximum: its (value, row) wins
+        const int src = __ffs(tie) - 1;
+        bi = __shfl_sync(0xffffffffu, bi, src);
+        bv = __shfl_sync(0xffffffffu, bv, src);
+      } else {
+        const uint32_t ml =
+            __reduce_max_sync(0xffffffffu, (cand && uint32_t(bits >> 32) == mh) ? uint32_t(bits) : 0u);
+        const bool win = cand && uint32_t(bits >> 32) == mh && uint32_t(bits) == ml;
+        bi = int(__reduce_min_sync(0xffffffffu, win ? uint32_t(bi) : 0xffffffffu));
+        bv = __hiloint2double(int(mh), int(ml));
+      }
+    }
+    if (!(bv > 0.0)) return false;
+    // the pivot (row bi before the swap); its reciprocal overlaps the swap
+    const double piv = A[bi * LP + cidx];
+    __syncwarp();
+    const double inv = 1.0 / piv;
+    if (bi != cidx) {
+      for (int b = lane; b <= m; b += 32) {
+        const double t0 = A[cidx * LP + b];
+        A[cidx * LP + b] = A[bi * LP + b];
+        A[bi * LP + b] = t0;
+      }
+    }
+    __syncwarp();
+    for (int a = cidx + 1 + lane; a < m; a += 32) {
+      const double l = A[a * LP + cidx] * inv;
+      A[a * LP + cidx] = l;
+      double* ra = A + a * LP;
+      const double* rc = A + cidx * LP;
+      int b = cidx + 1;
+      // 8 columns per batch: all loads issued before the FMAs (same arithmetic,
+      // eight independent shared-memory round trips in flight instead of one)
+      for (; b + 8 <= m + 1; b += 8) {
+        double x[8], y[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x[q] = rc[b + q];
+          y[q] = ra[b + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ra[b + q] = fma(-l, x[q], y[q]);
+      }
+      for (; b <= m; ++b) ra[b] = fma(-l, rc[b], ra[b]);
+    }
+    __syncwarp();
+  }
+  // back substitution in column (axpy) order, as dtrsm does it: the right-hand side
+  // lives in registers (lane k holds rows k, k + 32); per step one division on the
+  // owning lane, one broadcast, one FMA per remaining row.
+  double bq[NH];
+#pragma unroll
+  for (int q = 0; q < NH; ++q) {
+    const int k = lane + 32 * q;
+    bq[q] = k < m ? A[k * LP + m] : 0.0;
+  }
+  for (int a = m - 1; a >= 0; --a) {
+    const int src = a & 31, qa = a >> 5;
+    double mine = 0.0;
+#pragma unroll
+    for (int q = 0; q < NH; ++q)
+      if (q == qa) mine = bq[q];
+    const double xa = __shfl_sync(0xffffffffu, mine / A[a * LP + a], src);
+#pragma unroll
+    for (int q = 0; q < NH; ++q) {
+      const int k = lane + 32 * q;
+      if (k == a) bq[q] = xa;
+      else if (k < a) bq[q] = fma(-A[k * LP + a], xa, bq[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NH; ++q) {
+    const int k = lane + 32 * q;
+    if (k < m) A[k * LP + m] = bq[q];
+  }
+  __syncwarp();
+  return true;
+}
+
+// acc_i = sum_{j in P} M[i][j] x_j for every i, M given as M^T (lane i reads row j:
+// lane-consecutive addresses); x broadcast from the registers of its lanes.  Fully
+// unrolled over j so the shuffles and loads overlap (a loop over the set bits of P
+// was one dependent round trip per term).
+template <int RP>
+__device__ void bpp_matvec(const double* MT, int R, unsigned long long P, const double (&xs)[(RP + 31) / 32],
+                           double (&acc)[(RP + 31) / 32]) {
+  constexpr int NH = (RP + 31) / 32;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NH; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int j = 0; j < RP; ++j) {
+    const double xj = __shfl_sync(0xffffffffu, xs[j >> 5], j & 31);
+    if (j < R && ((P >> j) & 1ull)) {
+#pragma unroll
+      for (int q = 0; q < NH; ++q) {
+        const int i = lane + 32 * q;
+        if (i < R) acc[q] = fma(MT[j * R + i], xj, acc[q]);
+      }
+    }
+  }
+}
+
+// y = S[~P,P] x_P - f[~P] on the active indices, 0 on the passive ones (updaters.py:153-154)
+template <int RP>
+__device__ void bpp_dual(const double* S, int R, unsigned long long P, const double (&xs)[(RP + 31) / 32],
+                         const double (&fs)[(RP + 31) / 32], double (&ys)[(RP + 31) / 32]) {
+  constexpr int NH = (RP + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  double acc[NH];
+  bpp_matvec<RP>(S, R, P, xs, acc);
+#pragma unroll
+  for (int q = 0; q < NH; ++q) {
+    const int i = lane + 32 * q;
+    ys[q] = (i < R && !((P >> i) & 1ull)) ? acc[q] - fs[q] : 0.0;
+  }
+}
+
+// x, y for passive set P by the reference's direct solve: S[P,P] x_P = f_P (LU as
+// np.linalg.solve), y from S.  False when S[P,P] is singular.
+template <int RP>
+__device__ bool bpp_eval_direct(const double* S, int R, const double* fr, unsigned long long P, double* A, int* pidx,
+                                const double (&fs)[(RP + 31) / 32], double (&xs)[(RP + 31) / 32],
+                                double (&ys)[(RP + 31) / 32]) {
+  constexpr int NH = (RP + 31) / 32;
+  constexpr int LP = RP + 1;
+  const int lane = threadIdx.x & 31;
+  const int p = __popcll(P);
+#pragma unroll
+  for (int q = 0; q < NH; ++q) xs[q] = 0.0;
+  if (p > 0) {
+    // passive index list: variable r in P is the popc(P below r)-th entry
+    for (int r = lane; r < R; r += 32)
+      if ((P >> r) & 1ull) pidx[__popcll(P & ((1ull << r) - 1ull))] = r;
+    __syncwarp();
+    for (int a = lane; a < p; a += 32) {
+      const int ra = pidx[a];
+      for (int b = 0; b < p; ++b) A[a * LP + b] = S[pidx[b] * R + ra];   // S^T[pb][ra] = S[ra][pb]
+      A[a * LP + p] = fr[ra];
+    }
+    __syncwarp();
+    if (!warp_lu_solve<RP>(A, p, LP)) return false;
+#pragma unroll
+    for (int q = 0; q < NH; ++q) {
+      const int r = lane + 32 * q;
+      if (r < R && ((P >> r) & 1ull)) xs[q] = A[__popcll(P & ((1ull << r) - 1ull)) * LP + p];
+    }
+    __syncwarp();
+  }
+  bpp_dual<RP>(S, R, P, xs, fs, ys);
+  return true;
+}
+
+// Warp solve of a symmetric positive definite m x m system (pitch LP, rhs in column m)
+// by elimination without pivoting; the solution overwrites column m.  False when a
+// pivot is not positive (the caller then solves directly).
+__device__ bool warp_spd_solve(double* A, int m, int LP) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < m; ++c) {
+    const double piv = A[c * LP + c];
+    if (!(piv > 0.0)) return false;
+    const double inv = 1.0 / piv;
+    for (int a = c + 1 + lane; a < m; a += 32) {
+      const double l = A[a * LP + c] * inv;
+      for (int b = c + 1; b <= m; ++b) A[a * LP + b] = fma(-l, A[c * LP + b], A[a * LP + b]);
+    }
+    __syncwarp();
+  }
+  for (int a = m - 1; a >= 0; --a) {   // back substitution, one row per step
+    if (lane == 0) {
+      double v = A[a * LP + m];
+      for (int b = a + 1; b < m; ++b) v = fma(-A[a * LP + b], A[b * LP + m], v);
+      A[a * LP + m] = v / A[a * LP + a];
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// x for passive set P from T = S^-1 (held as T^T) when few variables are active
+// (q = R - p small): with Q the active set, the constrained solve is
+//   x = T f~ - T[:,Q] w,  T[Q,Q] w = (T f~)_Q     (f~ = f on P, 0 on Q)
+// -- block elimination of the KKT system: one q x q solve instead of a p x p one.
+// False when T[Q,Q] is not numerically positive definite (the caller solves directly).
+template <int RP>
+__device__ bool bpp_schur(const double* TT, int R, unsigned long long P, double* A, int* qidx, double* zbuf,
+                          const double (&rhs)[(RP + 31) / 32], double (&xs)[(RP + 31) / 32]) {
+  constexpr int NH = (RP + 31) / 32;
+  constexpr int LP = RP + 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long all = R < 64 ? ((1ull << R) - 1ull) : ~0ull;
+  const unsigned long long Q = all & ~P;
+  const int q = __popcll(Q);
+  double z[NH];
+  bpp_matvec<RP>(TT, R, P, rhs, z);     // z = T f~
+  if (q > 0) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      const int i = lane + 32 * k;
+      if (i < R) zbuf[i] = z[k];
+    }
+    for (int r = lane; r < R; r += 32)
+      if ((Q >> r) & 1ull) qidx[__popcll(Q & ((1ull << r) - 1ull))] = r;
+    __syncwarp();
+    for (int e = lane; e < q * q; e += 32) {
+      const int a = e / q, b = e - (e / q) * q;
+      A[a * LP + b] = TT[qidx[b] * R + qidx[a]];   // T[qa][qb]
+    }
+    for (int a = lane; a < q; a += 32) A[a * LP + q] = zbuf[qidx[a]];
+    __syncwarp();
+    if (!warp_spd_solve(A, q, LP)) return false;
+    for (int a = 0; a < q; ++a) {
+      const double wa = A[a * LP + q];
+      const int ra = qidx[a];
+#pragma unroll
+      for (int k = 0; k < NH; ++k) {
+        const int i = lane + 32 * k;
+        if (i < R) z[k] = fma(-TT[ra * R + i], wa, z[k]);   // T[i][ra]
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    const int i = lane + 32 * k;
+    xs[k] = (i < R && ((P >> i) & 1ull)) ? z[k] : 0.0;
+  }
+  return true;
+}
+
+// C = A B for R x R row-major shared-memory matrices, block-cooperative.
+__device__ void block_matmul(const double* Am, const double* Bm, double* C, int R) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e - (e / R) * R;
+    const double* ar = Am + i * R;
+    double s0 = 0.0, s1 = 0.0;
+    int k = 0;
+    for (; k + 2 <= R; k += 2) {
+      s0 = fma(ar[k], Bm[k * R + j], s0);
+      s1 = fma(ar[k + 1], Bm[(k + 1) * R + j], s1);
+    }
+    if (k < R) s0 = fma(ar[k], Bm[k * R + j], s0);
+    C[e] = s0 + s1;
+  }
+}
+
+// max |I - S T| over the entries, block-cooperative (S symmetric: S^T storage = S)
+__device__ double block_inv_residual(const double* S, const double* Tm, double* E, int R, double* red) {
+  block_matmul(S, Tm, E, R);
+  __syncthreads();
+  double mx = 0.0;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e - (e / R) * R;
+    const double v = (i == j ? 1.0 : 0.0) - E[e];
+    E[e] = v;
+    mx = fmax(mx, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  double m = 0.0;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+  __syncthreads();
+  return m;
+}
+
+// T^T = (S^-1)^T for the block-elimination passes.  Warm: Newton-Schulz from the
+// inverse the previous outer iteration left in `cache` (S changes little between
+// sweeps; T <- T + T (I - S T) squares the residual, 2-4 steps of two R^3 products);
+// cold or not converging: Gauss-Jordan on [S | I] without pivoting (S = Hadamard of
+// Grams is symmetric positive definite when nonsingular: the pivots are Schur
+// complements).  False (uniformly) when S is too close to singular for either: the
+// kernel then solves every pass directly.
+template <int RP>
+__device__ bool block_inverse(const double* S, int R, double* work, double* TT, double* gj, const double* cache,
+                              double* red) {
+  constexpr int W = 2 * RP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* Tm = work;                 // R x R, row-major
+  double* E = work + RP * RP;
+  double* Tn = work + 2 * RP * RP;
+  if (cache != nullptr && cache[R * R] == 1.0) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, j = e - (e / R) * R;
+      Tm[e] = cache[j * R + i];      // cache holds T^T
+    }
+    __syncthreads();
+    double err = block_inv_residual(S, Tm, E, R, red);
+    for (int step = 0; step < 4 && err > 1e-14 && err < 0.25; ++step) {
+      block_matmul(Tm, E, Tn, R);   // T E
+      __syncthreads();
+      for (int e = threadIdx.x; e < R * R; e += blockDim.x) Tm[e] += Tn[e];
+      __syncthreads();
+      const double prev = err;
+      err = block_inv_residual(S, Tm, E, R, red);
+      if (err > 0.5 * prev) break;  // stagnating at the rounding floor
+    }
+    if (err <= 1e-11) {
+      for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e - (e / R) * R;
+        TT[j * R + i] = Tm[e];
+      }
+      __syncthreads();
+      return true;
+    }
+  }
+  // Gauss-Jordan: [S | I] with row pitch 2 RP; warp w owns rows w, w + nw, ..., lanes
+  // walk columns (no integer division in the element loops)
+  double* aug = work;
+  double* rowbuf = gj;
+  double* colfac = gj + 2 * RP;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int i = warp; i < R; i += nw)
+    for (int j = lane; j < 2 * R; j += 32)
+      aug[i * W + j] = j < R ? S[j * R + i] : (j - R == i ? 1.0 : 0.0);
+  __syncthreads();
+  for (int c = 0; c < R; ++c) {
+    const double piv = aug[c * W + c];
+    if (!(piv > 1e-8 * fabs(S[c * R + c]))) {
+      if (threadIdx.x == 0) bad = 1;
+    }
+    __syncthreads();
+    if (bad) return false;
+    const double inv = 1.0 / piv;
+    for (int j = threadIdx.x; j < 2 * R; j += blockDim.x) rowbuf[j] = aug[c * W + j] * inv;
+    for (int i = threadIdx.x; i < R; i += blockDim.x) colfac[i] = aug[i * W + c];
+    __syncthreads();
+    for (int i = warp; i < R; i += nw) {
+      const double f = colfac[i];
+      for (int j = lane; j < 2 * R; j += 32)
+        aug[i * W + j] = (i == c) ? rowbuf[j] : fma(-f, rowbuf[j], aug[i * W + j]);
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < R; i += nw)
+    for (int j = lane; j < R; j += 32) TT[j * R + i] = aug[i * W + R + j];
+  __syncthreads();
+  return true;
+}
 
 template <int RP>
-__global__ void __launch_bounds__(kBppWarps * 32)
+__global__ void __launch_bounds__(bpp_warps<RP>() * 32)
     bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
-               int* status, unsigned int* ticket) {
+               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, double* tcache) {
   extern __shared__ __align__(16) double dsm[];
   constexpr int LP = RP + 1;  // LU pitch (augmented column at index p)
-  double* S = dsm;                                    // R*R
-  double* red = S + RP * RP;                          // kBppWarps * 64
-  double* colbuf = red + kBppWarps * 64;              // RP + 1
-  double* lu = colbuf + RP + 1;                       // kBppWarps * RP * LP
-  int* pidx_all = reinterpret_cast<int*>(lu + size_t(kBppWarps) * RP * LP);   // kBppWarps * 64
+  constexpr int NH = (RP + 31) / 32;  // entries per lane
+  constexpr int NW = bpp_warps<RP>();
+  double* S = dsm;                                    // RP*RP (holds S^T)
+  double* TT = S + RP * RP;                           // RP*RP (T^T, T = S^-1)
+  double* red = TT + RP * RP;                         // NW * 64
+  double* colbuf = red + NW * 64;                     // RP + 1
+  double* zall = colbuf + RP + 1;                     // NW * RP
+  double* gj = zall + NW * RP;                        // 3 * RP (Gauss-Jordan row / column buffers)
+  double* lu = gj + 3 * RP;                           // NW * RP * LP (the inverse's work space at the start)
+  int* pidx_all = reinterpret_cast<int*>(lu + size_t(NW) * RP * LP);   // NW * 64
+  int* qidx_all = pidx_all + NW * 64;                                  // NW * 64
+#ifdef NNCP_BPP_TIMING
+  const long long tk0 = clock64();
+#endif
   load_hadamard<true>(S, grams, order, mode, R);   // S^T: the gathers below walk columns across lanes
   __syncthreads();
+#ifdef NNCP_BPP_TIMING
+  const long long tk1 = clock64();
+#endif
+  // the block-elimination passes need S^-1; order 0 (an explicit S from bpp_update)
+  // need not be symmetric: solve those directly, like the reference
+  const bool t_ok = order > 0 && block_inverse<RP>(S, R, lu, TT, gj, tcache, red);
+#ifdef NNCP_BPP_TIMING
+  const long long tk2 = clock64();
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* A = lu + size_t(warp) * RP * LP;
   int* pidx = pidx_all + warp * 64;   // pidx[a] = index of the a-th passive variable
-  constexpr int NH = (RP + 31) / 32;  // entries per lane
+  int* qidx = qidx_all + warp * 64;   // qidx[a] = index of the a-th active variable
+  double* zbuf = zall + warp * RP;
   double xs[NH], ys[NH], fs[NH];
   double sq2[NH];
 #pragma unroll
   for (int q = 0; q < NH; ++q) sq2[q] = 0.0;
   double bsum = 0.0;
 
-  for (int64_t i = int64_t(blockIdx.x) * kBppWarps + warp; i < rows; i += int64_t(gridDim.x) * kBppWarps) {
+  // rows spread evenly over the CTAs (one or two per warp up to ~2400 rows): the kernel's
+  // latency is the per-CTA S^-1 plus one row's passes, so more CTAs, not more rows per CTA
+  const int64_t rpc = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t row_lo = int64_t(blockIdx.x) * rpc, row_hi = min(rows, row_lo + rpc);
+  for (int64_t i = row_lo + warp; i < row_hi; i += NW) {
     const double* fr = mrows + i * R;
 #pragma unroll
     for (int q = 0; q < NH; ++q) {
@@ -131,177 +528,71 @@ __global__ void __launch_bounds__(kBppWarps * 32)
       xs[q] = 0.0;
       ys[q] = -fs[q];
     }
+    // warm start (psets): the passive set this row ended with in the previous outer
+    // iteration.  The first pass then only evaluates it; the exchange rules below are
+    // the reference's from there on (the NNLS minimiser is unique for SPD S).  A row
+    // whose fast attempt (warm start and/or block-elimination passes) fails is redone
+    // exactly as the reference does it: cold start, direct solves -- so failures
+    // (BppCyclingError, singular solves) are the reference's.
+    const unsigned long long warm_set = psets ? psets[i] & (R < 64 ? ((1ull << R) - 1ull) : ~0ull) : 0ull;
     unsigned long long P = 0ull;
-    int best = R + 1, backup = 3;
     bool done = false;
     int fail_kind = 0;
-    for (int it = 0; it < 5 * R + 1; ++it) {
-      unsigned long long viol = 0ull;
+    for (int attempt = (warm_set != 0ull || t_ok) ? 0 : 1; attempt < 2 && !done; ++attempt) {
+      const bool fast = attempt == 0;
+      P = fast ? warm_set : 0ull;
 #pragma unroll
       for (int q = 0; q < NH; ++q) {
-        const int r = lane + 32 * q;
-        const bool pr = (P >> r) & 1ull;
-        const bool v = (r < R) && ((pr && xs[q] < 0.0) || (!pr && ys[q] < 0.0));
-        viol |= (unsigned long long)__ballot_sync(0xffffffffu, v) << (32 * q);
+        xs[q] = 0.0;
+        ys[q] = -fs[q];
       }
-      const int k = __popcll(viol);
-      if (k == 0) {
-        done = true;
-        break;
-      }
-      if (k < best) {
-        best = k;
-        backup = 3;
-        P ^= viol;
-      } else if (backup > 0) {
-        --backup;
-        P ^= viol;
-      } else {
-        P ^= 1ull << (63 - __clzll(viol));
-      }
-      // ---- solve S[P,P] x = f[P] (LU, partial pivoting), y = S[~P,P] x - f[~P]
-      const int p = __popcll(P);
-      // compact passive indices: idx[a] for a < p, built identically by every lane
-      // gather A (p x p) and rhs into this warp's scratch
-      // passive index list: variable r in P is the popc(P below r)-th entry
-      for (int r = lane; r < R; r += 32)
-        if ((P >> r) & 1ull) pidx[__popcll(P & ((1ull << r) - 1ull))] = r;
-      __syncwarp();
-      for (int a = lane; a < p; a += 32) {
-        const int ra = pidx[a];
-        for (int b = 0; b < p; ++b) A[a * LP + b] = S[pidx[b] * R + ra];   // S^T[pb][ra] = S[ra][pb]
-        A[a * LP + p] = fr[ra];
-      }
-      __syncwarp();
-      bool singular = false;
-      for (int cidx = 0; cidx < p; ++cidx) {
-        // pivot: max |A[i][c]| over i >= c, first index on ties (idamax).  Exact
-        // warp argmax in three reductions: |v| >= 0 orders like its bit pattern, so
-        // max of the high words, then of the low words among those, then the
-        // smallest row index among the exact maxima.
-        double bv = -1.0;
-        int bi = INT_MAX;
-        for (int a = cidx + lane; a < p; a += 32) {
-          const double v = fabs(A[a * LP + cidx]);
-          if (v > bv) {
-            bv = v;
-            bi = a;
-          }
-        }
-        {
-          const bool cand = bi != INT_MAX;
-          const unsigned long long bits = cand ? (unsigned long long)__double_as_longlong(bv) : 0ull;
-          const uint32_t mh = __reduce_max_sync(0xffffffffu, uint32_t(bits >> 32));
-          const unsigned tie = __ballot_sync(0xffffffffu, cand && uint32_t(bits >> 32) == mh);
-          if (__popc(tie) == 1) {   // one lane holds the high-word maximum: its (value, row) wins
-            const int src = __ffs(tie) - 1;
-            bi = __shfl_sync(0xffffffffu, bi, src);
-            bv = __shfl_sync(0xffffffffu, bv, src);
-          } else {
-            const uint32_t ml =
-                __reduce_max_sync(0xffffffffu, (cand && uint32_t(bits >> 32) == mh) ? uint32_t(bits) : 0u);
-            const bool win = cand && uint32_t(bits >> 32) == mh && uint32_t(bits) == ml;
-            bi = int(__reduce_min_sync(0xffffffffu, win ? uint32_t(bi) : 0xffffffffu));
-            bv = __hiloint2double(int(mh), int(ml));
-          }
-        }
-        if (!(bv > 0.0)) {
-          singular = true;
-          break;
-        }
-        // the pivot (row bi before the swap); its reciprocal overlaps the swap
-        const double piv = A[bi * LP + cidx];
-        __syncwarp();
-        const double inv = 1.0 / piv;
-        if (bi != cidx) {
-          for (int b = lane; b <= p; b += 32) {
-            const double t0 = A[cidx * LP + b];
-            A[cidx * LP + b] = A[bi * LP + b];
-            A[bi * LP + b] = t0;
-          }
-        }
-        __syncwarp();
-        for (int a = cidx + 1 + lane; a < p; a += 32) {
-          const double l = A[a * LP + cidx] * inv;
-          A[a * LP + cidx] = l;
-          double* ra = A + a * LP;
-          const double* rc = A + cidx * LP;
-          int b = cidx + 1;
-          // 8 columns per batch: all loads issued before the FMAs (same arithmetic,
-          // eight independent shared-memory round trips in flight instead of one)
-          for (; b + 8 <= p + 1; b += 8) {
-            double x[8], y[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              x[q] = rc[b + q];
-              y[q] = ra[b + q];
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) ra[b + q] = fma(-l, x[q], y[q]);
-          }
-          for (; b <= p; ++b) ra[b] = fma(-l, rc[b], ra[b]);
-        }
-        __syncwarp();
-      }
-      if (singular) {
-        fail_kind = 2;
-        break;
-      }
-      // back substitution in column (axpy) order, as dtrsm does it: the right-hand
-      // side lives in registers (lane k holds rows k, k + 32); per step one division
-      // on the owning lane, one broadcast, one FMA per remaining row -- no warp
-      // reduction on the sequential chain.  The solution overwrites column p.
-      {
-        double bq[NH];
-#pragma unroll
-        for (int q = 0; q < NH; ++q) {
-          const int k = lane + 32 * q;
-          bq[q] = k < p ? A[k * LP + p] : 0.0;
-        }
-        for (int a = p - 1; a >= 0; --a) {
-          const int src = a & 31, qa = a >> 5;
-          double mine = 0.0;
-#pragma unroll
-          for (int q = 0; q < NH; ++q)
-            if (q == qa) mine = bq[q];
-          const double xa = __shfl_sync(0xffffffffu, mine / A[a * LP + a], src);
+      bool pending = P != 0ull;       // x, y of P not evaluated yet
+      bool direct_only = !(fast && t_ok);
+      int best = R + 1, backup = 3;
+      fail_kind = 0;
+      for (int it = 0; it < 5 * R + 1; ++it) {
+        if (!pending) {
+          unsigned long long viol = 0ull;
 #pragma unroll
           for (int q = 0; q < NH; ++q) {
-            const int k = lane + 32 * q;
-            if (k == a) bq[q] = xa;
-            else if (k < a) bq[q] = fma(-A[k * LP + a], xa, bq[q]);
+            const int r = lane + 32 * q;
+            const bool pr = (P >> r) & 1ull;
+            const bool v = (r < R) && ((pr && xs[q] < 0.0) || (!pr && ys[q] < 0.0));
+            viol |= (unsigned long long)__ballot_sync(0xffffffffu, v) << (32 * q);
           }
-        }
-#pragma unroll
-        for (int q = 0; q < NH; ++q) {
-          const int k = lane + 32 * q;
-          if (k < p) A[k * LP + p] = bq[q];
-        }
-        __syncwarp();
-      }
-      // scatter x, compute y on the active set
-#pragma unroll
-      for (int q = 0; q < NH; ++q) {
-        const int r = lane + 32 * q;
-        xs[q] = 0.0;
-        ys[q] = 0.0;
-        if (r < R) {
-          if ((P >> r) & 1ull) {
-            const int a = __popcll(P & ((1ull << r) - 1ull));
-            xs[q] = A[a * LP + p];
+          const int k = __popcll(viol);
+          if (k == 0) {
+            done = true;
+            break;
+          }
+          if (k < best) {
+            best = k;
+            backup = 3;
+            P ^= viol;
+          } else if (backup > 0) {
+            --backup;
+            P ^= viol;
           } else {
-            double s = 0.0;
-            unsigned long long nn = P;
-            for (int b = 0; b < p; ++b) {
-              const int rb = __ffsll(nn) - 1;
-              nn &= nn - 1;
-              s = fma(S[rb * R + r], A[b * LP + p], s);   // S^T[rb][r] = S[r][rb]
-            }
-            ys[q] = s - fs[q];
+            P ^= 1ull << (63 - __clzll(viol));
           }
         }
+        pending = false;
+        // ---- x_P for the new passive set (updaters.py:152), y = S[~P,P] x_P - f[~P].
+        // Few active variables: block elimination through S^-1 (a q x q solve); many:
+        // the reference's direct solve of S[P,P] (a p x p solve).  Same minimiser.
+        const int p = __popcll(P);
+        if (!direct_only && 2 * p > R) {
+          if (bpp_schur<RP>(TT, R, P, A, qidx, zbuf, fs, xs)) {
+            bpp_dual<RP>(S, R, P, xs, fs, ys);
+            continue;
+          }
+          direct_only = true;     // T[Q,Q] not positive definite: this row continues directly
+        }
+        if (!bpp_eval_direct<RP>(S, R, fr, P, A, pidx, fs, xs, ys)) {
+          fail_kind = 2;
+          break;
+        }
       }
-      __syncwarp();
     }
     if (!done && fail_kind == 0) fail_kind = 1;
     if (fail_kind) {
@@ -310,6 +601,7 @@ __global__ void __launch_bounds__(kBppWarps * 32)
         atomicMax(status + 3, fail_kind);
       }
     }
+    if (psets && lane == 0) psets[i] = fail_kind ? 0ull : P;
     double* hr = hhat + i * R;
 #pragma unroll
     for (int q = 0; q < NH; ++q) {
@@ -322,8 +614,20 @@ __global__ void __launch_bounds__(kBppWarps * 32)
 #pragma unroll
     for (int q = 0; q < NH; ++q) sq2[q] = fma(xs[q], xs[q], sq2[q]);
   }
+#ifdef NNCP_BPP_TIMING
+  const long long tk3 = clock64();
+#endif
   __syncthreads();
-  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket);
+  // every CTA holds the same S^-1 (identical inputs and arithmetic); the last CTA
+  // publishes it for the next outer iteration's warm Newton-Schulz start (tcache:
+  // R x R entries + a valid flag), after every CTA has read the old one
+  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket, TT, tcache, tcache ? R * R : 0,
+                      t_ok ? 1.0 : 0.0);
+#ifdef NNCP_BPP_TIMING
+  if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("bpp cta %d warp %d t_ok %d: hadamard %lld inverse %lld rows %lld epilogue %lld\n", blockIdx.x,
+           warp, int(t_ok), tk1 - tk0, tk2 - tk1, tk3 - tk2, clock64() - tk3);
+#endif
 }
 
 // --------------------------------------------------- normalise + Gram ------
@@ -604,7 +908,7 @@ size_t row_update_part_elems(int64_t rows, int rank) {
 
 int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
            const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
-           size_t ws_bytes, cudaStream_t st, double mu_eps) {
+           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, double* bpp_tcache) {
   if (rows <= 0) {
     // an empty row block still owes its (zero) column sums
     if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
@@ -626,15 +930,17 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
           grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
           mu_eps);
   } else if (algo == NNCP_ALGO_BPP) {
-    const int blocks = int(std::min<int64_t>((rows + kBppWarps - 1) / kBppWarps, int64_t(num_sms()) * 4));
-    if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
     NNCP_RP_CASES(rp, {
-      const size_t smem = sizeof(double) * (size_t(RP) * RP + kBppWarps * 64 + RP + 1 +
-                                            size_t(kBppWarps) * RP * (RP + 1)) +
-                          sizeof(int) * kBppWarps * 64;
+      constexpr int NW = bpp_warps<RP>();
+      const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms())));
+      if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
+      const size_t smem = sizeof(double) * (2 * size_t(RP) * RP + NW * 64 + RP + 1 + NW * RP + 3 * RP +
+                                            size_t(NW) * RP * (RP + 1)) +
+                          sizeof(int) * NW * 128;
       if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;
-      bpp_kernel<RP><<<blocks, kBppWarps * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
-                                                           beta, status, w.tickets + T_UPDATE);
+      bpp_kernel<RP><<<blocks, NW * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
+                                                           beta, status, w.tickets + T_UPDATE,
+                                                           static_cast<unsigned long long*>(bpp_sets), bpp_tcache);
     });
   } else {
     return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");

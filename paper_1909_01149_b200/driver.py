@@ -81,6 +81,11 @@ class RunConfig:
     # M >= J, dimtree.py:25-39); "auto" = that rule, except that the sliced engine
     # takes the split minimising M + J when it at least halves it
     dimtree_split: str = "auto"
+    # ANLS-BPP: start each row's block principal pivoting from the passive set it ended
+    # with in the previous outer iteration instead of P = {} (updaters.py:121-155).  The
+    # minimiser is unique for SPD S and the final pass solves on the final passive set,
+    # so the result is the reference's; False = the reference's cold start every time.
+    bpp_warm_start: bool = True
 
     def validate(self, order: int):
         if self.rank < 1:
@@ -469,6 +474,12 @@ class _Engine:
         self.me = layout.rank if layout is not None else 0
         self.xvec = torch.zeros(1 + self.nranks * N, **f64)
         self.masks = torch.zeros(2 * N, dtype=torch.int32, device=dev)
+        # BPP: every owned row's final passive set, the next outer iteration's start
+        # (nncp_update_ex; same final solve as the reference's cold start, fewer passes)
+        self.bpp_sets = ([torch.zeros(max(self.n_owned[n], 1), dtype=torch.int64, device=dev) for n in range(N)]
+                         if cfg.algorithm == "bpp" and cfg.bpp_warm_start else None)
+        # and each mode's S^-1 (+ valid flag) for the next sweep's Newton-Schulz warm start
+        self.bpp_tcache = ([torch.zeros(R * R + 1, **f64) for _ in range(N)] if self.bpp_sets else None)
         fault = os.environ.get(_FAULT_ENV)
         self.fault = tuple(int(v) for v in fault.split(":")) if fault else None
         self.mbar = torch.empty((max(self.dims), R), **f64)
@@ -590,11 +601,13 @@ class _Engine:
             self._cmark("ReduceScatter")
             last = n == N - 1
             if cfg.algorithm in FUSED_ALGORITHMS:
-                _lib.check(lib.nncp_update(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
-                                           _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
-                                           _lib.ptr(self.hhat), _lib.ptr(self.nsq),
-                                           _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]),
-                                           self.ws.ptr, self.ws.nbytes, st))
+                _lib.check(lib.nncp_update_ex(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
+                                              _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
+                                              _lib.ptr(self.hhat), _lib.ptr(self.nsq),
+                                              _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]),
+                                              1e-16, _lib.ptr(self.bpp_sets[n]) if self.bpp_sets else None,
+                                              _lib.ptr(self.bpp_tcache[n]) if self.bpp_sets else None,
+                                              self.ws.ptr, self.ws.nbytes, st))
             else:
                 self._iterative_update(n, m_owned, last)
             self.timer.mark("NNLS")
