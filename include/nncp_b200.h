@@ -165,11 +165,14 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank,
  *   bpp_tcache device double[rank*rank + 1]: S^-1 of the previous call for this mode and
  *              a valid flag (zero-filled = none); refreshed in place.  With it the
  *              per-CTA inverse behind the block-elimination passes (few active variables)
- *              is a Newton-Schulz correction instead of a Gauss-Jordan elimination. */
+ *              is a Newton-Schulz correction instead of a Gauss-Jordan elimination.
+ * m_ld: 0 = mttkrp_rows is row-major (rows x rank); > 0 = column-major with that
+ * leading dimension (>= rows), i.e. the dimension tree's temporary (dimtree.py:68-99)
+ * consumed in place, without the np.ascontiguousarray transpose (dimtree.py:287). */
 int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, void* ws, size_t ws_bytes,
-                   void* stream);
+                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t m_ld, void* ws,
+                   size_t ws_bytes, void* stream);
 
 /* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
  * gram = owned^T owned (raw, local rows).  owned may alias hhat; lam and gram may be NULL. */
@@ -191,6 +194,15 @@ int nncp_normalize_from_gram(const double* hhat, const double* gram_raw, int64_t
 /* driver.py:368,431 gamma = lam^T (prod_m sym(G_m)) lam over all `order` Grams. */
 int nncp_gamma(const double* grams, int order, int rank, const double* lam, double* gamma,
                void* stream);
+/* nncp_normalize_gram for the sweep's last mode, whose last CTA then also does
+ * nncp_gamma_publish (grams: all `order` Grams, this mode's being the one written):
+ * one launch instead of two when no All-Reduce of the Gram sits in between (a
+ * single context). */
+int nncp_normalize_gram_publish(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned,
+                                double* lam, double* gram, void* ws, size_t ws_bytes, const double* grams, int order,
+                                double* gamma_out, int* status, int count, double* codes, int nslots, int offset,
+                                int* masks_out, void* stream);
+
 /* The same gamma, plus the end-of-sweep status hand-off (grid.py:172-203 failure
  * propagation).  codes[0..nslots) is a rank-slotted vector: every slot is zeroed, then
  * for n < count codes[offset + n] = kind * 2^32 + failing row of status n (0 when the

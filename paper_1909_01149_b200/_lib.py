@@ -69,12 +69,15 @@ SIGNATURES = [
       ctypes.c_size_t, vp]),
     ("nncp_update_ex", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
-      ctypes.c_double, vp, vp, vp, ctypes.c_size_t, vp]),
+      ctypes.c_double, vp, vp, ctypes.c_int64, vp, ctypes.c_size_t, vp]),
     ("nncp_normalize_gram", ctypes.c_int,
      [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gram", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gamma", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
     ("nncp_normalize_from_gram", ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
+    ("nncp_normalize_gram_publish", ctypes.c_int,
+     [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_int, vp, vp, ctypes.c_int,
+      vp, ctypes.c_int, ctypes.c_int, vp, vp]),
     ("nncp_gamma_publish", ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int,
                                           ctypes.c_int, vp, vp]),
     ("nncp_inner", ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),

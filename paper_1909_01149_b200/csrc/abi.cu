@@ -28,18 +28,20 @@ int multi_ttv(const double*, int, const int64_t*, int, int, const double* const*
 int temp_to_rows(const double*, int64_t, int, double*, cudaStream_t);
 int khatri_rao(const double* const*, const int64_t*, int, int, double*, cudaStream_t);
 int update(int, const double*, int, int, int, const double*, const double*, const double*, int64_t, double*, double*,
-           double*, int*, void*, size_t, cudaStream_t, double, void*, double*);
+           double*, int*, void*, size_t, cudaStream_t, double, void*, double*, int64_t);
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
 int normalize_from_gram(const double*, const double*, int64_t, int, double*, double*, double*, cudaStream_t);
 int gamma_publish(const double*, int, int, const double*, double*, int*, int, double*, int, int, int*, cudaStream_t);
+int normalize_gram_publish(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t,
+                           const double*, int, double*, int*, int, double*, int, int, int*, cudaStream_t);
 int inner(const double*, const double*, const double*, int64_t, int, double*, void*, size_t, cudaStream_t);
 int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
 int status_reset(int*, int, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
 int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
-        cudaStream_t);
+        cudaStream_t, int64_t);
 int admm_step(const double*, int, int, int, double, const double*, const double*, double*, double*, int64_t, double*,
               int*, void*, size_t, cudaStream_t);
 int nes_hyper(const double*, int, int, int, double, double*, cudaStream_t);
@@ -229,8 +231,9 @@ int nncp_status_reset_n(int* status, int count, void* stream) {
 
 int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t m_ld, void* ws,
+                   size_t ws_bytes, void* stream) {
+  if (m_ld < 0 || (m_ld > 0 && m_ld < rows)) return fail(NNCP_ERR_VALUE, "m_ld must be 0 (row-major) or >= rows");
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
   if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
@@ -241,17 +244,17 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
       if (beta) NNCP_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), S(stream)));
       return NNCP_OK;
     }
-    return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream));
+    return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream), m_ld);
   }
   return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
-                S(stream), mu_eps, bpp_sets, bpp_tcache);
+                S(stream), mu_eps, bpp_sets, bpp_tcache, m_ld);
 }
 
 int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                 const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
                 int* status, void* ws, size_t ws_bytes, void* stream) {
   return nncp_update_ex(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status,
-                        1e-16, nullptr, nullptr, ws, ws_bytes, stream);   // MU_EPSILON, updaters.py:27; BPP cold
+                        1e-16, nullptr, nullptr, 0, ws, ws_bytes, stream);   // MU_EPSILON (updaters.py:27)
 }
 
 int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
@@ -277,6 +280,19 @@ int nncp_normalize_from_gram(const double* hhat, const double* gram_raw, int64_t
   if (!gram_raw) return fail(NNCP_ERR_VALUE, "raw gram required");
   if (gram == gram_raw) return fail(NNCP_ERR_VALUE, "gram output must not alias the raw gram");
   return normalize_from_gram(hhat, gram_raw, rows, rank, owned, lam, gram, S(stream));
+}
+
+int nncp_normalize_gram_publish(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned,
+                                double* lam, double* gram, void* ws, size_t ws_bytes, const double* grams, int order,
+                                double* gamma_out, int* status, int count, double* codes, int nslots, int offset,
+                                int* masks_out, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  if (!nsq || !gram || !grams || !gamma_out || !status || !codes)
+    return fail(NNCP_ERR_VALUE, "nsq, gram, grams, gamma, status and codes are required");
+  if (count < 0 || count > kMaxOrder) return fail(NNCP_ERR_VALUE, "status count must be in [0, max order]");
+  if (offset < 0 || offset + count > nslots) return fail(NNCP_ERR_VALUE, "status slot outside the codes vector");
+  return normalize_gram_publish(hhat, nsq, rows, rank, owned, lam, gram, ws, ws_bytes, grams, order, gamma_out, status,
+                                count, codes, nslots, offset, masks_out, S(stream));
 }
 
 int nncp_gamma_publish(const double* grams, int order, int rank, const double* lam, double* gamma_out, int* status,

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
                        const double* __restrict__ mrows, const double* __restrict__ owned,
                        const double* __restrict__ lam, int64_t rows, double* __restrict__ hhat,
                        double* __restrict__ part, double* nsq, double* beta, int* status, unsigned int* ticket,
-                       double mu_eps) {
+                       double mu_eps, int64_t mld) {
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     for (int q = 0; q < 2; ++q) {
       const int r = lane + 32 * q;
       h[q] = (r < R) ? (lam ? orow[r] * lam[r] : orow[r]) : 0.0;  // driver.py:403 current = owned * lam
-      m[q] = (r < R) ? mr[r] : 0.0;
+      // M row-major, or (mld > 0) the dimension tree's column-major temporary itself
+      m[q] = (r < R) ? (mld ? mrows[i + mld * r] : mr[r]) : 0.0;
     }
     if (ALGO == NNCP_ALGO_MU) {
       // updaters.py:93-94: current * M / (current @ S + eps)
@@ -476,7 +477,8 @@ template <int RP>
 __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
     bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
-               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, double* tcache) {
+               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, double* tcache,
+               int64_t mld) {
   extern __shared__ __align__(16) double dsm[];
   constexpr int LP = RP + 1;  // LU pitch (augmented column at index p)
   constexpr int NH = (RP + 31) / 32;  // entries per lane
@@ -487,7 +489,8 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   double* colbuf = red + NW * 64;                     // RP + 1
   double* zall = colbuf + RP + 1;                     // NW * RP
   double* gj = zall + NW * RP;                        // 3 * RP (Gauss-Jordan row / column buffers)
-  double* lu = gj + 3 * RP;                           // NW * RP * LP (the inverse's work space at the start)
+  double* fall = gj + 3 * RP;                         // NW * RP (each warp's right-hand side f)
+  double* lu = fall + NW * RP;                        // NW * RP * LP (the inverse's work space at the start)
   int* pidx_all = reinterpret_cast<int*>(lu + size_t(NW) * RP * LP);   // NW * 64
   int* qidx_all = pidx_all + NW * 64;                                  // NW * 64
 #ifdef NNCP_BPP_TIMING
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   int* pidx = pidx_all + warp * 64;   // pidx[a] = index of the a-th passive variable
   int* qidx = qidx_all + warp * 64;   // qidx[a] = index of the a-th active variable
   double* zbuf = zall + warp * RP;
+  double* fbuf = fall + warp * RP;
   double xs[NH], ys[NH], fs[NH];
   double sq2[NH];
 #pragma unroll
@@ -520,14 +524,17 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   const int64_t rpc = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t row_lo = int64_t(blockIdx.x) * rpc, row_hi = min(rows, row_lo + rpc);
   for (int64_t i = row_lo + warp; i < row_hi; i += NW) {
-    const double* fr = mrows + i * R;
+    // f = this row of M: row-major, or (mld > 0) the dimension tree's column-major temporary
 #pragma unroll
     for (int q = 0; q < NH; ++q) {
       const int r = lane + 32 * q;
-      fs[q] = (r < R) ? fr[r] : 0.0;
+      fs[q] = (r < R) ? (mld ? mrows[i + mld * r] : mrows[i * R + r]) : 0.0;
       xs[q] = 0.0;
       ys[q] = -fs[q];
+      if (r < R) fbuf[r] = fs[q];
     }
+    __syncwarp();
+    const double* fr = fbuf;
     // warm start (psets): the passive set this row ended with in the previous outer
     // iteration.  The first pass then only evaluates it; the exchange rules below are
     // the reference's from there on (the NNLS minimiser is unique for SPD S).  A row
@@ -630,6 +637,68 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 #endif
 }
 
+// ------------------------------------------------------------- scalars -----
+// End-of-sweep scalars: gamma = lam^T (prod_m sym(G_m)) lam (driver.py:431), and the
+// status hand-off.  codes[0..nslots) is the rank-slotted vector that one SUM
+// All-Reduce combines: every slot is zeroed, then this rank's slot [offset, offset +
+// count) gets, per mode, failure kind * 2^32 + failing row (0 = none; exact in fp64);
+// masks[2n..2n+1] = the warning bits; the status words are reset for the next sweep
+// (the reset the caller would otherwise launch separately).  Block-cooperative;
+// W (R*R) and v (R) are shared-memory scratch.
+struct PublishArgs {
+  const double* grams;
+  int order;
+  const double* lam;
+  double* gamma;
+  int* status;
+  int count;
+  double* codes;
+  int nslots;
+  int offset;
+  int* masks;
+};
+
+__device__ void gamma_publish_body(const PublishArgs& a, int R, double* W, double* v) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e / R, c = e - (e / R) * R;
+    double p = 1.0;
+    for (int m = 0; m < a.order; ++m) {
+      const double* g = a.grams + size_t(m) * R * R;
+      const double sym = 0.5 * (g[r * R + c] + g[c * R + r]);
+      p = (m == 0) ? sym : p * sym;
+    }
+    W[e] = p * a.lam[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int c = 0; c < R; ++c) s += W[threadIdx.x * R + c];
+    v[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(a.lam[k], v[k], s);
+    a.gamma[0] = s;
+  }
+  if (a.status == nullptr) return;
+  for (int e = threadIdx.x; e < a.nslots; e += blockDim.x) a.codes[e] = 0.0;
+  __syncthreads();
+  if (int(threadIdx.x) < a.count) {
+    int* st = a.status + threadIdx.x * NNCP_STATUS_WORDS;
+    const int kind = st[3], row = st[2];
+    a.codes[a.offset + threadIdx.x] = kind ? double(kind) * 4294967296.0 + double(row) : 0.0;
+    if (a.masks != nullptr) {
+      a.masks[2 * threadIdx.x] = st[0];
+      a.masks[2 * threadIdx.x + 1] = st[1];
+    }
+    st[0] = 0;
+    st[1] = 0;
+    st[2] = INT_MAX;
+    st[3] = 0;
+  }
+}
+
 // --------------------------------------------------- normalise + Gram ------
 constexpr int kGramRows = 64;
 
@@ -637,7 +706,7 @@ template <int RP>
 __global__ void __launch_bounds__(256)
     normalize_gram_kernel(const double* __restrict__ hhat, const double* __restrict__ nsq, int64_t rows, int R,
                           double* __restrict__ owned, double* __restrict__ lam, double* __restrict__ gram,
-                          double* __restrict__ part, unsigned int* ticket) {
+                          double* __restrict__ part, unsigned int* ticket, const PublishArgs pub) {
   __shared__ double tile[kGramRows * RP];
   __shared__ double scale[RP];
   if (threadIdx.x < R) {
@@ -685,7 +754,16 @@ __global__ void __launch_bounds__(256)
     for (int o = 0; o < 4; ++o)
       if (e0 + o * int(blockDim.x) < RR) mypart[e0 + o * blockDim.x] = s[o];
   }
-  if (last_cta_ticket(ticket)) finish_partials(part, gridDim.x, RR, gram);
+  if (last_cta_ticket(ticket)) {
+    finish_partials(part, gridDim.x, RR, gram);
+    if (pub.gamma != nullptr) {
+      // the sweep's last normalisation also produces gamma and hands the status off
+      // (a single context: no All-Reduce of the Gram in between) -- one launch fewer
+      __threadfence();
+      __syncthreads();
+      gamma_publish_body(pub, R, tile, scale);
+    }
+  }
 }
 
 // Normalisation from the All-Reduced Gram of the UNnormalised rows (the grid path's
@@ -714,56 +792,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// ------------------------------------------------------------- scalars -----
-__global__ void __launch_bounds__(256)
-    gamma_kernel(const double* __restrict__ grams, int order, int R, const double* __restrict__ lam,
-                 double* __restrict__ gamma, int* status = nullptr, int count = 0, double* codes = nullptr,
-                 int nslots = 0, int offset = 0, int* masks = nullptr) {
+__global__ void __launch_bounds__(256) gamma_kernel(const PublishArgs a, int R) {
   __shared__ double W[kMaxRank * kMaxRank];
   __shared__ double v[kMaxRank];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int a = e / R, b = e - (e / R) * R;
-    double p = 1.0;
-    for (int m = 0; m < order; ++m) {
-      const double* g = grams + size_t(m) * R * R;
-      const double sym = 0.5 * (g[a * R + b] + g[b * R + a]);
-      p = (m == 0) ? sym : p * sym;
-    }
-    W[e] = p * lam[b];
-  }
-  __syncthreads();
-  if (threadIdx.x < R) {
-    double s = 0.0;
-    for (int b = 0; b < R; ++b) s += W[threadIdx.x * R + b];
-    v[threadIdx.x] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < R; ++k) s = fma(lam[k], v[k], s);
-    gamma[0] = s;
-  }
-  // end of sweep: publish this context's update status and reset it for the next sweep
-  // (the reset the caller would otherwise launch separately).  codes[0..nslots) is the
-  // rank-slotted vector that one SUM All-Reduce combines: every slot is zeroed, then
-  // this rank's slot [offset, offset + count) gets, per mode, failure kind * 2^32 +
-  // failing row (0 = none; exact in fp64); masks[2n..2n+1] = the warning bits.
-  if (status == nullptr) return;
-  for (int e = threadIdx.x; e < nslots; e += blockDim.x) codes[e] = 0.0;
-  __syncthreads();
-  if (threadIdx.x < count) {
-    int* st = status + threadIdx.x * NNCP_STATUS_WORDS;
-    const int kind = st[3], row = st[2];
-    codes[offset + threadIdx.x] = kind ? double(kind) * 4294967296.0 + double(row) : 0.0;
-    if (masks != nullptr) {
-      masks[2 * threadIdx.x] = st[0];
-      masks[2 * threadIdx.x + 1] = st[1];
-    }
-    st[0] = 0;
-    st[1] = 0;
-    st[2] = INT_MAX;
-    st[3] = 0;
-  }
+  gamma_publish_body(a, R, W, v);
 }
 
 __global__ void __launch_bounds__(256)
@@ -908,7 +940,7 @@ size_t row_update_part_elems(int64_t rows, int rank) {
 
 int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
            const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
-           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, double* bpp_tcache) {
+           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t mld) {
   if (rows <= 0) {
     // an empty row block still owes its (zero) column sums
     if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
@@ -924,23 +956,24 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
     if (algo == NNCP_ALGO_MU)
       update_rows_kernel<NNCP_ALGO_MU><<<blocks, kRowWarps * 32, 0, st>>>(
           grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps);
+          mu_eps, mld);
     else
       update_rows_kernel<NNCP_ALGO_HALS><<<blocks, kRowWarps * 32, 0, st>>>(
           grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps);
+          mu_eps, mld);
   } else if (algo == NNCP_ALGO_BPP) {
     NNCP_RP_CASES(rp, {
       constexpr int NW = bpp_warps<RP>();
       const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms())));
       if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
-      const size_t smem = sizeof(double) * (2 * size_t(RP) * RP + NW * 64 + RP + 1 + NW * RP + 3 * RP +
+      const size_t smem = sizeof(double) * (2 * size_t(RP) * RP + NW * 64 + RP + 1 + 2 * NW * RP + 3 * RP +
                                             size_t(NW) * RP * (RP + 1)) +
                           sizeof(int) * NW * 128;
       if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;
       bpp_kernel<RP><<<blocks, NW * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
                                                            beta, status, w.tickets + T_UPDATE,
-                                                           static_cast<unsigned long long*>(bpp_sets), bpp_tcache);
+                                                           static_cast<unsigned long long*>(bpp_sets), bpp_tcache,
+                                                           mld);
     });
   } else {
     return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");
@@ -949,17 +982,24 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
   return NNCP_OK;
 }
 
-int normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
-                   double* gram, void* ws, size_t ws_bytes, cudaStream_t st, int ticket_slot) {
+static int normalize_gram_impl(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
+                   double* gram, void* ws, size_t ws_bytes, cudaStream_t st, int ticket_slot,
+                   const PublishArgs* pub) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int rp = pad8(rank);
   const int blocks = int(std::max<int64_t>(1, (rows + kGramRows - 1) / kGramRows));
   if (gram && w.part_elems < size_t(blocks) * rank * rank) return fail(NNCP_ERR_VALUE, "workspace too small (gram)");
   NNCP_RP_CASES(rp, (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
                                                                       owned, lam, gram, w.part,
-                                                                      w.tickets + ticket_slot)));
+                                                                      w.tickets + ticket_slot,
+                                                                      pub ? *pub : PublishArgs{})));
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
+}
+
+int normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
+                   double* gram, void* ws, size_t ws_bytes, cudaStream_t st, int ticket_slot) {
+  return normalize_gram_impl(hhat, nsq, rows, rank, owned, lam, gram, ws, ws_bytes, st, ticket_slot, nullptr);
 }
 
 int normalize_from_gram(const double* hhat, const double* graw, int64_t rows, int rank, double* owned, double* lam,
@@ -972,14 +1012,24 @@ int normalize_from_gram(const double* hhat, const double* graw, int64_t rows, in
 }
 
 int gamma(const double* grams, int order, int rank, const double* lam, double* out, cudaStream_t st) {
-  gamma_kernel<<<1, 256, 0, st>>>(grams, order, rank, lam, out);
+  PublishArgs a{grams, order, lam, out, nullptr, 0, nullptr, 0, 0, nullptr};
+  gamma_kernel<<<1, 256, 0, st>>>(a, rank);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }
 
+int normalize_gram_publish(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,
+                           double* gram, void* ws, size_t ws_bytes, const double* grams, int order, double* gamma_out,
+                           int* status, int count, double* codes, int nslots, int offset, int* masks,
+                           cudaStream_t st) {
+  PublishArgs a{grams, order, lam, gamma_out, status, count, codes, nslots, offset, masks};
+  return normalize_gram_impl(hhat, nsq, rows, rank, owned, lam, gram, ws, ws_bytes, st, 2, &a);
+}
+
 int gamma_publish(const double* grams, int order, int rank, const double* lam, double* out, int* status, int count,
                   double* codes, int nslots, int offset, int* masks, cudaStream_t st) {
-  gamma_kernel<<<1, 256, 0, st>>>(grams, order, rank, lam, out, status, count, codes, nslots, offset, masks);
+  PublishArgs a{grams, order, lam, out, status, count, codes, nslots, offset, masks};
+  gamma_kernel<<<1, 256, 0, st>>>(a, rank);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

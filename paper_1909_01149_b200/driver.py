@@ -590,9 +590,18 @@ class _Engine:
         cfg = self.cfg
         if cfg.use_dimtree:
             self.ctx.begin_iteration()
+        # a single context hands the tree's column-major result to the fused update as
+        # is (m_ld); grids need row blocks for the Reduce-Scatter
+        in_place = not self.coll.parallel and cfg.algorithm in FUSED_ALGORITHMS
+        published = False
         for n in range(N):
             mb = self.mbar[: self.dims[n]]
-            if cfg.use_dimtree:
+            m_ld = 0
+            if in_place:
+                temp = (self.ctx.mttkrp(self.x, self.shared, n, rows=False) if cfg.use_dimtree
+                        else self.ctx.mttkrp_direct(self.x, self.shared, n, rows=False))
+                mb, m_ld = temp.data, self.dims[n]
+            elif cfg.use_dimtree:
                 self.ctx.mttkrp(self.x, self.shared, n, out=mb)
             else:
                 self.ctx.mttkrp_direct(self.x, self.shared, n, out=mb)
@@ -606,7 +615,7 @@ class _Engine:
                                               _lib.ptr(self.hhat), _lib.ptr(self.nsq),
                                               _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]),
                                               1e-16, _lib.ptr(self.bpp_sets[n]) if self.bpp_sets else None,
-                                              _lib.ptr(self.bpp_tcache[n]) if self.bpp_sets else None,
+                                              _lib.ptr(self.bpp_tcache[n]) if self.bpp_sets else None, m_ld,
                                               self.ws.ptr, self.ws.nbytes, st))
             else:
                 self._iterative_update(n, m_owned, last)
@@ -625,6 +634,16 @@ class _Engine:
                                                         R, _lib.ptr(self.owned[n]), _lib.ptr(self.lam),
                                                         _lib.ptr(self.grams[n]), st))
                 self.timer.mark("NNLS")
+            elif last and not self.coll.parallel:
+                # a single context: the last normalisation also computes gamma and hands
+                # the status words off (nncp_gamma_publish folded in, one launch fewer)
+                _lib.check(lib.nncp_normalize_gram_publish(
+                    _lib.ptr(self.hhat), _lib.ptr(self.nsq), self.n_owned[n], R, _lib.ptr(self.owned[n]),
+                    _lib.ptr(self.lam), _lib.ptr(self.grams[n]), self.ws.ptr, self.ws.nbytes, _lib.ptr(self.grams), N,
+                    _lib.vp(self.scal.data_ptr() + 8), _lib.ptr(self.status), N, _lib.vp(self.xvec.data_ptr() + 8),
+                    self.nranks * N, self.me * N, _lib.ptr(self.masks), st))
+                self.timer.mark("Gram")
+                published = True
             else:
                 self.coll.all_reduce(self.nsq)
                 self._cmark("AllReduce")
@@ -636,11 +655,12 @@ class _Engine:
                 self._cmark("AllReduce")
             self._gather(n)
             self._cmark("AllGather")
-        _lib.check(lib.nncp_gamma_publish(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam),
-                                          _lib.vp(self.scal.data_ptr() + 8), _lib.ptr(self.status), N,
-                                          _lib.vp(self.xvec.data_ptr() + 8), self.nranks * N, self.me * N,
-                                          _lib.ptr(self.masks), st))
-        self.timer.mark("Error")
+        if not published:
+            _lib.check(lib.nncp_gamma_publish(_lib.ptr(self.grams), N, R, _lib.ptr(self.lam),
+                                              _lib.vp(self.scal.data_ptr() + 8), _lib.ptr(self.status), N,
+                                              _lib.vp(self.xvec.data_ptr() + 8), self.nranks * N, self.me * N,
+                                              _lib.ptr(self.masks), st))
+            self.timer.mark("Error")
         self.coll.all_reduce(self.xvec, words=1)      # beta + every rank's status codes
         self._cmark("AllReduce")
         self.host_xvec.copy_(self.xvec, non_blocking=True)
@@ -803,6 +823,17 @@ class _Engine:
     @property
     def graph(self):
         return self.graphs[0][0] if self.graphs else None
+
+    def set_timing(self, enabled: bool):
+        """Turn the per-category CUDA events on or off for the following sweeps (the
+        sweep graphs are re-captured without / with their event-record nodes; each
+        costs ~1-2 us of GPU timeline, which matters for the smallest tensors)."""
+        enabled = bool(enabled)
+        if enabled == self.timer.enabled:
+            return
+        self.timer.enabled = enabled
+        self.ctx.marker = self.timer.mark if enabled else None
+        self.graphs = []
 
     def _capture_graphs(self):
         """Two copies of the sweep graph with their own timing events, replayed alternately:

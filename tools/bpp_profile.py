@@ -40,7 +40,7 @@ def main():
         _lib.check(lib.nncp_status_reset(_lib.ptr(status), st))
         _lib.check(lib.nncp_update_ex(3, _lib.ptr(dg), order, order - 1, r, _lib.ptr(dm), _lib.ptr(cur), None, rows,
                                       _lib.ptr(out), None, None, _lib.ptr(status), 1e-16,
-                                      _lib.ptr(sets) if k % 2 else None, _lib.ptr(tcache) if k % 2 else None,
+                                      _lib.ptr(sets) if k % 2 else None, _lib.ptr(tcache) if k % 2 else None, 0,
                                       _lib.vp(ws.data_ptr()), ws.numel(), st))
         ev[2 * k + 1].record()
     torch.cuda.synchronize()
