@@ -156,23 +156,19 @@ int nncp_update(int algo, const double* grams, int order, int mode, int rank,
                 double* hhat, double* nsq, double* beta, int* status, void* ws, size_t ws_bytes,
                 void* stream);
 /* nncp_update with extra inputs.  mu_eps: the MU epsilon (mu_update(inp, eps),
- * updaters.py:91-94; nncp_update uses MU_EPSILON = 1e-16, updaters.py:27).  BPP only
- * (both may be NULL: the reference's cold start):
- *   bpp_sets   device uint64[rows]: per row the passive-set bit mask to start from,
- *              overwritten with the final one (0 after a failure).  The NNLS minimiser is
- *              unique for SPD S, so a warm start from the previous outer iteration's sets
- *              reaches the same solution in fewer passes;
- *   bpp_tcache device double[rank*rank + 1]: S^-1 of the previous call for this mode and
- *              a valid flag (zero-filled = none); refreshed in place.  With it the
- *              per-CTA inverse behind the block-elimination passes (few active variables)
- *              is a Newton-Schulz correction instead of a Gauss-Jordan elimination.
- * m_ld: 0 = mttkrp_rows is row-major (rows x rank); > 0 = column-major with that
- * leading dimension (>= rows), i.e. the dimension tree's temporary (dimtree.py:68-99)
- * consumed in place, without the np.ascontiguousarray transpose (dimtree.py:287). */
+ * updaters.py:91-94; nncp_update uses MU_EPSILON = 1e-16, updaters.py:27).
+ * bpp_sets (BPP only, may be NULL = the reference's cold start from P = {}): device
+ * uint64[rows], per row the passive-set bit mask to start from, overwritten with the
+ * final one (0 after a failure).  The NNLS minimiser is unique for SPD S, so a warm
+ * start from the previous outer iteration's sets reaches the same solution in fewer
+ * passes.  m_ld: 0 = mttkrp_rows is row-major (rows x rank); > 0 = column-major with
+ * that leading dimension (>= rows), i.e. the dimension tree's temporary
+ * (dimtree.py:68-99) consumed in place, without the np.ascontiguousarray transpose
+ * (dimtree.py:287). */
 int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t m_ld, void* ws,
-                   size_t ws_bytes, void* stream);
+                   int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
+                   void* stream);
 
 /* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
  * gram = owned^T owned (raw, local rows).  owned may alias hhat; lam and gram may be NULL. */

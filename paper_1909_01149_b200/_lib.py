@@ -69,7 +69,7 @@ SIGNATURES = [
       ctypes.c_size_t, vp]),
     ("nncp_update_ex", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
-      ctypes.c_double, vp, vp, ctypes.c_int64, vp, ctypes.c_size_t, vp]),
+      ctypes.c_double, vp, ctypes.c_int64, vp, ctypes.c_size_t, vp]),
     ("nncp_normalize_gram", ctypes.c_int,
      [vp, vp, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_gram", ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]),

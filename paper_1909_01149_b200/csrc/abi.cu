@@ -28,7 +28,7 @@ int multi_ttv(const double*, int, const int64_t*, int, int, const double* const*
 int temp_to_rows(const double*, int64_t, int, double*, cudaStream_t);
 int khatri_rao(const double* const*, const int64_t*, int, int, double*, cudaStream_t);
 int update(int, const double*, int, int, int, const double*, const double*, const double*, int64_t, double*, double*,
-           double*, int*, void*, size_t, cudaStream_t, double, void*, double*, int64_t);
+           double*, int*, void*, size_t, cudaStream_t, double, void*, int64_t);
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
@@ -231,8 +231,8 @@ int nncp_status_reset_n(int* status, int count, void* stream) {
 
 int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                   int* status, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t m_ld, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
+                   void* stream) {
   if (m_ld < 0 || (m_ld > 0 && m_ld < rows)) return fail(NNCP_ERR_VALUE, "m_ld must be 0 (row-major) or >= rows");
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
@@ -247,14 +247,14 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
     return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream), m_ld);
   }
   return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
-                S(stream), mu_eps, bpp_sets, bpp_tcache, m_ld);
+                S(stream), mu_eps, bpp_sets, m_ld);
 }
 
 int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                 const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
                 int* status, void* ws, size_t ws_bytes, void* stream) {
   return nncp_update_ex(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status,
-                        1e-16, nullptr, nullptr, 0, ws, ws_bytes, stream);   // MU_EPSILON (updaters.py:27)
+                        1e-16, nullptr, 0, ws, ws_bytes, stream);   // MU_EPSILON (updaters.py:27)
 }
 
 int nncp_normalize_gram(const double* hhat, const double* nsq, int64_t rows, int rank, double* owned, double* lam,

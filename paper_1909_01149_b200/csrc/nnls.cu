@@ -359,90 +359,19 @@ __device__ bool bpp_schur(const double* TT, int R, unsigned long long P, double*
   return true;
 }
 
-// C = A B for R x R row-major shared-memory matrices, block-cooperative.
-__device__ void block_matmul(const double* Am, const double* Bm, double* C, int R) {
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, j = e - (e / R) * R;
-    const double* ar = Am + i * R;
-    double s0 = 0.0, s1 = 0.0;
-    int k = 0;
-    for (; k + 2 <= R; k += 2) {
-      s0 = fma(ar[k], Bm[k * R + j], s0);
-      s1 = fma(ar[k + 1], Bm[(k + 1) * R + j], s1);
-    }
-    if (k < R) s0 = fma(ar[k], Bm[k * R + j], s0);
-    C[e] = s0 + s1;
-  }
-}
-
-// max |I - S T| over the entries, block-cooperative (S symmetric: S^T storage = S)
-__device__ double block_inv_residual(const double* S, const double* Tm, double* E, int R, double* red) {
-  block_matmul(S, Tm, E, R);
-  __syncthreads();
-  double mx = 0.0;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, j = e - (e / R) * R;
-    const double v = (i == j ? 1.0 : 0.0) - E[e];
-    E[e] = v;
-    mx = fmax(mx, fabs(v));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  double m = 0.0;
-  for (int w = 0; w < int(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
-  __syncthreads();
-  return m;
-}
-
-// T^T = (S^-1)^T for the block-elimination passes.  Warm: Newton-Schulz from the
-// inverse the previous outer iteration left in `cache` (S changes little between
-// sweeps; T <- T + T (I - S T) squares the residual, 2-4 steps of two R^3 products);
-// cold or not converging: Gauss-Jordan on [S | I] without pivoting (S = Hadamard of
-// Grams is symmetric positive definite when nonsingular: the pivots are Schur
-// complements).  False (uniformly) when S is too close to singular for either: the
-// kernel then solves every pass directly.
+// T^T = (S^-1)^T for the block-elimination passes, by Gauss-Jordan on [S | I] without
+// pivoting (S = Hadamard of Grams is symmetric positive definite when nonsingular: the
+// pivots are Schur complements).  Block-cooperative, two barriers per step; returns
+// false (uniformly) when a pivot is not comfortably positive -- the kernel then solves
+// every pass directly.  (A Newton-Schulz refresh from the previous sweep's inverse was
+// measured slower: S moves by 1e-2..1 between sweeps early on, and each R^3 product in
+// shared memory cost about as much as the whole elimination.)
 template <int RP>
-__device__ bool block_inverse(const double* S, int R, double* work, double* TT, double* gj, const double* cache,
-                              double* red) {
-  constexpr int W = 2 * RP;
+__device__ bool block_inverse(const double* S, int R, double* aug, double* TT, double* gj) {
+  constexpr int W = 2 * RP;   // [S | I] with row pitch 2 RP; warp w owns rows w, w + nw, ...
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* Tm = work;                 // R x R, row-major
-  double* E = work + RP * RP;
-  double* Tn = work + 2 * RP * RP;
-  if (cache != nullptr && cache[R * R] == 1.0) {
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int i = e / R, j = e - (e / R) * R;
-      Tm[e] = cache[j * R + i];      // cache holds T^T
-    }
-    __syncthreads();
-    double err = block_inv_residual(S, Tm, E, R, red);
-    for (int step = 0; step < 4 && err > 1e-14 && err < 0.25; ++step) {
-      block_matmul(Tm, E, Tn, R);   // T E
-      __syncthreads();
-      for (int e = threadIdx.x; e < R * R; e += blockDim.x) Tm[e] += Tn[e];
-      __syncthreads();
-      const double prev = err;
-      err = block_inv_residual(S, Tm, E, R, red);
-      if (err > 0.5 * prev) break;  // stagnating at the rounding floor
-    }
-    if (err <= 1e-11) {
-      for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-        const int i = e / R, j = e - (e / R) * R;
-        TT[j * R + i] = Tm[e];
-      }
-      __syncthreads();
-      return true;
-    }
-  }
-  // Gauss-Jordan: [S | I] with row pitch 2 RP; warp w owns rows w, w + nw, ..., lanes
-  // walk columns (no integer division in the element loops)
-  double* aug = work;
-  double* rowbuf = gj;
-  double* colfac = gj + 2 * RP;
+  double* rowbuf = gj;        // 2 RP: the scaled pivot row
+  double* colfac = gj + 2 * RP;   // RP: the pivot column before the step
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   for (int i = warp; i < R; i += nw)
@@ -451,15 +380,12 @@ __device__ bool block_inverse(const double* S, int R, double* work, double* TT, 
   __syncthreads();
   for (int c = 0; c < R; ++c) {
     const double piv = aug[c * W + c];
-    if (!(piv > 1e-8 * fabs(S[c * R + c]))) {
-      if (threadIdx.x == 0) bad = 1;
-    }
-    __syncthreads();
-    if (bad) return false;
     const double inv = 1.0 / piv;
+    if (threadIdx.x == 0 && !(piv > 1e-8 * fabs(S[c * R + c]))) bad = 1;
     for (int j = threadIdx.x; j < 2 * R; j += blockDim.x) rowbuf[j] = aug[c * W + j] * inv;
     for (int i = threadIdx.x; i < R; i += blockDim.x) colfac[i] = aug[i * W + c];
     __syncthreads();
+    if (bad) return false;
     for (int i = warp; i < R; i += nw) {
       const double f = colfac[i];
       for (int j = lane; j < 2 * R; j += 32)
@@ -477,8 +403,7 @@ template <int RP>
 __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
     bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
-               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, double* tcache,
-               int64_t mld) {
+               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, int64_t mld) {
   extern __shared__ __align__(16) double dsm[];
   constexpr int LP = RP + 1;  // LU pitch (augmented column at index p)
   constexpr int NH = (RP + 31) / 32;  // entries per lane
@@ -503,7 +428,7 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 #endif
   // the block-elimination passes need S^-1; order 0 (an explicit S from bpp_update)
   // need not be symmetric: solve those directly, like the reference
-  const bool t_ok = order > 0 && block_inverse<RP>(S, R, lu, TT, gj, tcache, red);
+  const bool t_ok = order > 0 && block_inverse<RP>(S, R, lu, TT, gj);
 #ifdef NNCP_BPP_TIMING
   const long long tk2 = clock64();
 #endif
@@ -625,11 +550,7 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   const long long tk3 = clock64();
 #endif
   __syncthreads();
-  // every CTA holds the same S^-1 (identical inputs and arithmetic); the last CTA
-  // publishes it for the next outer iteration's warm Newton-Schulz start (tcache:
-  // R x R entries + a valid flag), after every CTA has read the old one
-  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket, TT, tcache, tcache ? R * R : 0,
-                      t_ok ? 1.0 : 0.0);
+  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket);
 #ifdef NNCP_BPP_TIMING
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("bpp cta %d warp %d t_ok %d: hadamard %lld inverse %lld rows %lld epilogue %lld\n", blockIdx.x,
@@ -940,7 +861,7 @@ size_t row_update_part_elems(int64_t rows, int rank) {
 
 int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
            const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
-           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, double* bpp_tcache, int64_t mld) {
+           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, int64_t mld) {
   if (rows <= 0) {
     // an empty row block still owes its (zero) column sums
     if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
@@ -972,8 +893,7 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
       if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;
       bpp_kernel<RP><<<blocks, NW * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
                                                            beta, status, w.tickets + T_UPDATE,
-                                                           static_cast<unsigned long long*>(bpp_sets), bpp_tcache,
-                                                           mld);
+                                                           static_cast<unsigned long long*>(bpp_sets), mld);
     });
   } else {
     return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");

@@ -128,9 +128,7 @@ constexpr int kRowWarps = 8;
 // Per-CTA column sums of squares (+ beta) -> partials, last CTA reduces in order.
 template <int NH>
 __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, double* red /* [nw][64] */,
-                                double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket,
-                                const double* pub_src = nullptr, double* pub_dst = nullptr, int pub_n = 0,
-                                double pub_flag = 0.0) {
+                                double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 #pragma unroll
   for (int q = 0; q < NH; ++q) red[warp * 64 + lane + 32 * q] = sq[q];
@@ -157,12 +155,6 @@ __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, doub
       } else if (beta) {
         beta[0] = colbuf[e];
       }
-    }
-    // publish a per-CTA-identical shared-memory result for the next launch (every CTA
-    // has passed its prologue once the last ticket is taken)
-    if (pub_dst != nullptr) {
-      for (int e = threadIdx.x; e < pub_n; e += blockDim.x) pub_dst[e] = pub_src[e];
-      if (threadIdx.x == 0) pub_dst[pub_n] = pub_flag;
     }
   }
 }

@@ -478,8 +478,6 @@ class _Engine:
         # (nncp_update_ex; same final solve as the reference's cold start, fewer passes)
         self.bpp_sets = ([torch.zeros(max(self.n_owned[n], 1), dtype=torch.int64, device=dev) for n in range(N)]
                          if cfg.algorithm == "bpp" and cfg.bpp_warm_start else None)
-        # and each mode's S^-1 (+ valid flag) for the next sweep's Newton-Schulz warm start
-        self.bpp_tcache = ([torch.zeros(R * R + 1, **f64) for _ in range(N)] if self.bpp_sets else None)
         fault = os.environ.get(_FAULT_ENV)
         self.fault = tuple(int(v) for v in fault.split(":")) if fault else None
         self.mbar = torch.empty((max(self.dims), R), **f64)
@@ -615,8 +613,7 @@ class _Engine:
                                               _lib.ptr(self.hhat), _lib.ptr(self.nsq),
                                               _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]),
                                               1e-16, _lib.ptr(self.bpp_sets[n]) if self.bpp_sets else None,
-                                              _lib.ptr(self.bpp_tcache[n]) if self.bpp_sets else None, m_ld,
-                                              self.ws.ptr, self.ws.nbytes, st))
+                                              m_ld, self.ws.ptr, self.ws.nbytes, st))
             else:
                 self._iterative_update(n, m_owned, last)
             self.timer.mark("NNLS")

@@ -118,7 +118,7 @@ def _run(algo: str, inp: UpdateInputs, mu_eps: float = MU_EPSILON):
     st = _lib.stream_handle()
     _lib.check(lib.nncp_status_reset(_lib.ptr(status), st))
     _lib.check(lib.nncp_update_ex(_lib.ALGO_CODES[algo], _lib.ptr(s), 0, -1, r, _lib.ptr(m), _lib.ptr(cur), None,
-                                  rows, _lib.ptr(out), None, None, _lib.ptr(status), float(mu_eps), None, None, 0,
+                                  rows, _lib.ptr(out), None, None, _lib.ptr(status), float(mu_eps), None, 0,
                                   ws.ptr, ws.nbytes, st))
     raise_for_status(status.cpu().tolist(), algo)
     return to_host_if(out, host)

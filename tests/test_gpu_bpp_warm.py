@@ -1,7 +1,7 @@
 """ANLS-BPP on the device (bpp_kernel): each row's block principal
 pivoting starts from the passive set it ended with in the previous outer iteration
 (RunConfig.bpp_warm_start, default on), and a pass with few active variables solves
-through S^-1 (Newton-Schulz-refreshed across sweeps) by block elimination instead of a
+through S^-1 (Gauss-Jordan once per CTA) by block elimination instead of a
 full LU of S[P,P].  The NNLS minimiser is unique for SPD S, so warm and cold starts
 agree to rounding (bitwise when every pass is a direct solve), and both match the
 reference's golden runs and the oracle; a row whose fast attempt fails is redone with

@@ -32,7 +32,6 @@ def main():
     status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device="cuda")
     ws = torch.zeros(1 << 22, dtype=torch.uint8, device="cuda")
     sets = torch.zeros(rows, dtype=torch.int64, device="cuda")
-    tcache = torch.zeros(r * r + 1, dtype=torch.float64, device="cuda")
     st = _lib.stream_handle()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
     for k in range(reps):
@@ -40,7 +39,7 @@ def main():
         _lib.check(lib.nncp_status_reset(_lib.ptr(status), st))
         _lib.check(lib.nncp_update_ex(3, _lib.ptr(dg), order, order - 1, r, _lib.ptr(dm), _lib.ptr(cur), None, rows,
                                       _lib.ptr(out), None, None, _lib.ptr(status), 1e-16,
-                                      _lib.ptr(sets) if k % 2 else None, _lib.ptr(tcache) if k % 2 else None, 0,
+                                      _lib.ptr(sets) if k % 2 else None, 0,
                                       _lib.vp(ws.data_ptr()), ws.numel(), st))
         ev[2 * k + 1].record()
     torch.cuda.synchronize()
