@@ -169,6 +169,19 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
                    int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
                    void* stream);
+/* nncp_update_ex followed, in the same launch, by the normalisation of
+ * nncp_normalize_gram (driver.py:411-422) for a single context: the kernel's last CTA
+ * turns the column sums into w = sqrt(nsq), writes owned = hhat / (w > 0 ? w : 1),
+ * lam = w (owned / lam may be the inputs: they are read before the last CTA starts)
+ * and gram_out = H^T H of the normalised rows; with gamma_out it also does
+ * nncp_gamma_publish over status_all (the sweep's `status_count` per-mode blocks;
+ * grams: all `order` Grams, this mode's being gram_out).  Small
+ * row blocks only (one CTA does it; the host keeps rows * rank^2 <= 2^20), rank <= 32. */
+int nncp_update_normalize(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                          double* owned, double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                          int* status, double mu_eps, void* bpp_sets, int64_t m_ld, double* gram_out, double* gamma_out,
+                          int* status_all, int status_count, double* codes, int nslots, int offset, int* masks_out,
+                          void* ws, size_t ws_bytes, void* stream);
 
 /* driver.py:414-420: w = sqrt(nsq); owned = hhat / (w > 0 ? w : 1); lam = w;
  * gram = owned^T owned (raw, local rows).  owned may alias hhat; lam and gram may be NULL. */

@@ -67,6 +67,10 @@ SIGNATURES = [
     ("nncp_update", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp,
       ctypes.c_size_t, vp]),
+    ("nncp_update_normalize", ctypes.c_int,
+     [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
+      ctypes.c_double, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp,
+      ctypes.c_size_t, vp]),
     ("nncp_update_ex", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
       ctypes.c_double, vp, ctypes.c_int64, vp, ctypes.c_size_t, vp]),

@@ -4,7 +4,7 @@
 #include <atomic>
 #include <string>
 
-#include "common.cuh"
+#include "nnls_common.cuh"
 
 namespace nncp {
 
@@ -28,7 +28,7 @@ int multi_ttv(const double*, int, const int64_t*, int, int, const double* const*
 int temp_to_rows(const double*, int64_t, int, double*, cudaStream_t);
 int khatri_rao(const double* const*, const int64_t*, int, int, double*, cudaStream_t);
 int update(int, const double*, int, int, int, const double*, const double*, const double*, int64_t, double*, double*,
-           double*, int*, void*, size_t, cudaStream_t, double, void*, int64_t);
+           double*, int*, void*, size_t, cudaStream_t, double, void*, int64_t, const TailArgs*);
 int normalize_gram(const double*, const double*, int64_t, int, double*, double*, double*, void*, size_t, cudaStream_t,
                    int);
 int gamma(const double*, int, int, const double*, double*, cudaStream_t);
@@ -41,7 +41,7 @@ int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaSt
 int status_reset(int*, int, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
 int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
-        cudaStream_t, int64_t);
+        cudaStream_t, int64_t, const TailArgs*);
 int admm_step(const double*, int, int, int, double, const double*, const double*, double*, double*, int64_t, double*,
               int*, void*, size_t, cudaStream_t);
 int nes_hyper(const double*, int, int, int, double, double*, cudaStream_t);
@@ -229,10 +229,10 @@ int nncp_status_reset_n(int* status, int count, void* stream) {
   return status_reset(status, count, S(stream));
 }
 
-int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
-                   const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
-                   int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
-                   void* stream) {
+static int update_dispatch(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                           const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq,
+                           double* beta, int* status, double mu_eps, void* bpp_sets, int64_t m_ld, const TailArgs* tail,
+                           void* ws, size_t ws_bytes, void* stream) {
   if (m_ld < 0 || (m_ld > 0 && m_ld < rows)) return fail(NNCP_ERR_VALUE, "m_ld must be 0 (row-major) or >= rows");
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
@@ -244,10 +244,42 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
       if (beta) NNCP_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), S(stream)));
       return NNCP_OK;
     }
-    return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream), m_ld);
+    return ucp(grams, order, mode, rank, mttkrp_rows, rows, hhat, nsq, beta, status, ws, ws_bytes, S(stream), m_ld,
+               tail);
   }
   return update(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, ws, ws_bytes,
-                S(stream), mu_eps, bpp_sets, m_ld);
+                S(stream), mu_eps, bpp_sets, m_ld, tail);
+}
+
+int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                   const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                   int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
+                   void* stream) {
+  return update_dispatch(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, mu_eps,
+                         bpp_sets, m_ld, nullptr, ws, ws_bytes, stream);
+}
+
+int nncp_update_normalize(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
+                          double* owned, double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
+                          int* status, double mu_eps, void* bpp_sets, int64_t m_ld, double* gram_out, double* gamma_out,
+                          int* status_all, int status_count, double* codes, int nslots, int offset, int* masks_out,
+                          void* ws, size_t ws_bytes, void* stream) {
+  if (rank > 32) return fail(NNCP_ERR_UNSUPPORTED, "the fused normalisation takes rank <= 32");
+  if (rows < 1) return fail(NNCP_ERR_VALUE, "the fused normalisation needs rows");
+  if (!owned || !lam || !nsq || !gram_out || order < 1) return fail(NNCP_ERR_VALUE, "owned, lam, nsq and gram required");
+  if (gamma_out && (!codes || !status_all || status_count < 0 || status_count > kMaxOrder || offset < 0 ||
+                    offset + status_count > nslots))
+    return fail(NNCP_ERR_VALUE, "bad status hand-off arguments");
+  TailArgs t{};
+  t.hhat = hhat;
+  t.rows = rows;
+  t.owned = owned;
+  t.lam = lam;
+  t.gram = gram_out;
+  t.pub = PublishArgs{grams, order, lam, gamma_out, gamma_out ? status_all : nullptr, status_count, codes, nslots,
+                      offset, masks_out};
+  return update_dispatch(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, mu_eps,
+                         bpp_sets, m_ld, &t, ws, ws_bytes, stream);
 }
 
 int nncp_update(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
                        const double* __restrict__ mrows, const double* __restrict__ owned,
                        const double* __restrict__ lam, int64_t rows, double* __restrict__ hhat,
                        double* __restrict__ part, double* nsq, double* beta, int* status, unsigned int* ticket,
-                       double mu_eps, int64_t mld) {
+                       double mu_eps, int64_t mld, TailArgs tail) {
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
       }
     }
   }
-  colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket);
+  tail.scratch = S;   // S is dead after the rows
+  colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail);
 }
 
 // ------------------------------------------------------------------ BPP ----
@@ -403,7 +404,8 @@ template <int RP>
 __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
     bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
-               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, int64_t mld) {
+               int* status, unsigned int* ticket, unsigned long long* __restrict__ psets, int64_t mld,
+               TailArgs tail) {
   extern __shared__ __align__(16) double dsm[];
   constexpr int LP = RP + 1;  // LU pitch (augmented column at index p)
   constexpr int NH = (RP + 31) / 32;  // entries per lane
@@ -550,74 +552,13 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   const long long tk3 = clock64();
 #endif
   __syncthreads();
-  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket);
+  tail.scratch = lu;   // the per-warp scratch is dead after the rows
+  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail);
 #ifdef NNCP_BPP_TIMING
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("bpp cta %d warp %d t_ok %d: hadamard %lld inverse %lld rows %lld epilogue %lld\n", blockIdx.x,
            warp, int(t_ok), tk1 - tk0, tk2 - tk1, tk3 - tk2, clock64() - tk3);
 #endif
-}
-
-// ------------------------------------------------------------- scalars -----
-// End-of-sweep scalars: gamma = lam^T (prod_m sym(G_m)) lam (driver.py:431), and the
-// status hand-off.  codes[0..nslots) is the rank-slotted vector that one SUM
-// All-Reduce combines: every slot is zeroed, then this rank's slot [offset, offset +
-// count) gets, per mode, failure kind * 2^32 + failing row (0 = none; exact in fp64);
-// masks[2n..2n+1] = the warning bits; the status words are reset for the next sweep
-// (the reset the caller would otherwise launch separately).  Block-cooperative;
-// W (R*R) and v (R) are shared-memory scratch.
-struct PublishArgs {
-  const double* grams;
-  int order;
-  const double* lam;
-  double* gamma;
-  int* status;
-  int count;
-  double* codes;
-  int nslots;
-  int offset;
-  int* masks;
-};
-
-__device__ void gamma_publish_body(const PublishArgs& a, int R, double* W, double* v) {
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int r = e / R, c = e - (e / R) * R;
-    double p = 1.0;
-    for (int m = 0; m < a.order; ++m) {
-      const double* g = a.grams + size_t(m) * R * R;
-      const double sym = 0.5 * (g[r * R + c] + g[c * R + r]);
-      p = (m == 0) ? sym : p * sym;
-    }
-    W[e] = p * a.lam[c];
-  }
-  __syncthreads();
-  if (threadIdx.x < R) {
-    double s = 0.0;
-    for (int c = 0; c < R; ++c) s += W[threadIdx.x * R + c];
-    v[threadIdx.x] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < R; ++k) s = fma(a.lam[k], v[k], s);
-    a.gamma[0] = s;
-  }
-  if (a.status == nullptr) return;
-  for (int e = threadIdx.x; e < a.nslots; e += blockDim.x) a.codes[e] = 0.0;
-  __syncthreads();
-  if (int(threadIdx.x) < a.count) {
-    int* st = a.status + threadIdx.x * NNCP_STATUS_WORDS;
-    const int kind = st[3], row = st[2];
-    a.codes[a.offset + threadIdx.x] = kind ? double(kind) * 4294967296.0 + double(row) : 0.0;
-    if (a.masks != nullptr) {
-      a.masks[2 * threadIdx.x] = st[0];
-      a.masks[2 * threadIdx.x + 1] = st[1];
-    }
-    st[0] = 0;
-    st[1] = 0;
-    st[2] = INT_MAX;
-    st[3] = 0;
-  }
 }
 
 // --------------------------------------------------- normalise + Gram ------
@@ -861,7 +802,8 @@ size_t row_update_part_elems(int64_t rows, int rank) {
 
 int update(int algo, const double* grams, int order, int mode, int rank, const double* mrows, const double* owned,
            const double* lam, int64_t rows, double* hhat, double* nsq, double* beta, int* status, void* ws,
-           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, int64_t mld) {
+           size_t ws_bytes, cudaStream_t st, double mu_eps, void* bpp_sets, int64_t mld, const TailArgs* tail) {
+  const TailArgs tl = tail ? *tail : TailArgs{};
   if (rows <= 0) {
     // an empty row block still owes its (zero) column sums
     if (nsq) NNCP_CUDA_TRY(cudaMemsetAsync(nsq, 0, sizeof(double) * rank, st));
@@ -877,11 +819,11 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
     if (algo == NNCP_ALGO_MU)
       update_rows_kernel<NNCP_ALGO_MU><<<blocks, kRowWarps * 32, 0, st>>>(
           grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps, mld);
+          mu_eps, mld, tl);
     else
       update_rows_kernel<NNCP_ALGO_HALS><<<blocks, kRowWarps * 32, 0, st>>>(
           grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps, mld);
+          mu_eps, mld, tl);
   } else if (algo == NNCP_ALGO_BPP) {
     NNCP_RP_CASES(rp, {
       constexpr int NW = bpp_warps<RP>();
@@ -893,7 +835,7 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
       if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;
       bpp_kernel<RP><<<blocks, NW * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq,
                                                            beta, status, w.tickets + T_UPDATE,
-                                                           static_cast<unsigned long long*>(bpp_sets), mld);
+                                                           static_cast<unsigned long long*>(bpp_sets), mld, tl);
     });
   } else {
     return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");

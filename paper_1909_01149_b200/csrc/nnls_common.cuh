@@ -121,6 +121,128 @@ inline WsLayout ws_layout(void* ws, size_t bytes) {
 }
 enum Ticket { T_NORM = 0, T_UPDATE = 1, T_NORMGRAM = 2, T_GRAM = 3, T_INNER = 4, T_ITER = 5, T_COLSQ = 6 };
 
+// ------------------------------------------------------------- scalars -----
+// End-of-sweep scalars: gamma = lam^T (prod_m sym(G_m)) lam (driver.py:431), and the
+// status hand-off.  codes[0..nslots) is the rank-slotted vector that one SUM
+// All-Reduce combines: every slot is zeroed, then this rank's slot [offset, offset +
+// count) gets, per mode, failure kind * 2^32 + failing row (0 = none; exact in fp64);
+// masks[2n..2n+1] = the warning bits; the status words are reset for the next sweep
+// (the reset the caller would otherwise launch separately).  Block-cooperative;
+// W (R*R) and v (R) are shared-memory scratch.
+struct PublishArgs {
+  const double* grams;
+  int order;
+  const double* lam;
+  double* gamma;
+  int* status;
+  int count;
+  double* codes;
+  int nslots;
+  int offset;
+  int* masks;
+};
+
+static __device__ void gamma_publish_body(const PublishArgs& a, int R, double* W, double* v) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e / R, c = e - (e / R) * R;
+    double p = 1.0;
+    for (int m = 0; m < a.order; ++m) {
+      const double* g = a.grams + size_t(m) * R * R;
+      const double sym = 0.5 * (g[r * R + c] + g[c * R + r]);
+      p = (m == 0) ? sym : p * sym;
+    }
+    W[e] = p * a.lam[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int c = 0; c < R; ++c) s += W[threadIdx.x * R + c];
+    v[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(a.lam[k], v[k], s);
+    a.gamma[0] = s;
+  }
+  if (a.status == nullptr) return;
+  for (int e = threadIdx.x; e < a.nslots; e += blockDim.x) a.codes[e] = 0.0;
+  __syncthreads();
+  if (int(threadIdx.x) < a.count) {
+    int* st = a.status + threadIdx.x * NNCP_STATUS_WORDS;
+    const int kind = st[3], row = st[2];
+    a.codes[a.offset + threadIdx.x] = kind ? double(kind) * 4294967296.0 + double(row) : 0.0;
+    if (a.masks != nullptr) {
+      a.masks[2 * threadIdx.x] = st[0];
+      a.masks[2 * threadIdx.x + 1] = st[1];
+    }
+    st[0] = 0;
+    st[1] = 0;
+    st[2] = INT_MAX;
+    st[3] = 0;
+  }
+}
+
+// Single-context fusion of the normalisation into the update kernel's last CTA
+// (driver.py:411-422 after the column sums): w = sqrt(nsq), owned = hhat / (w > 0 ? w
+// : 1), lam = w, gram = H^T H of the normalised rows (rows staged 64 at a time in
+// `scratch`), and for the sweep's last mode also gamma + the status hand-off.  Only
+// for small row blocks (the host checks rows * R^2): one CTA does it all, in place
+// of the normalise (+ gamma) launches.
+struct TailArgs {
+  const double* hhat;     // nullptr: no fused tail
+  int64_t rows;
+  double* owned;
+  double* lam;
+  double* gram;
+  double* scratch;        // >= max(64 R, R^2 + R) doubles of shared memory
+  PublishArgs pub;        // pub.gamma == nullptr: no gamma / hand-off
+};
+
+static __device__ void fused_tail(const TailArgs& t, int R, const double* nsq_s /* shared, R */, double* scale) {
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    const double w = sqrt(nsq_s[r]);
+    scale[r] = (w > 0.0) ? w : 1.0;
+    if (t.lam) t.lam[r] = w;
+  }
+  __syncthreads();
+  const int RR = R * R;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};     // entries threadIdx.x + k * blockDim.x
+  double* tile = t.scratch;
+  for (int64_t r0 = 0; r0 < t.rows; r0 += 64) {
+    const int nr = int(t.rows - r0 < 64 ? t.rows - r0 : 64);
+    for (int e = threadIdx.x; e < nr * R; e += blockDim.x) {
+      const int il = e / R, c = e - (e / R) * R;
+      const int64_t gi = (r0 + il) * R + c;
+      const double v = t.hhat[gi] / scale[c];
+      t.owned[gi] = v;
+      tile[il * R + c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < RR) {
+        const int a = e / R, b = e - (e / R) * R;
+        double sacc = acc[k];
+        for (int il = 0; il < nr; ++il) sacc = fma(tile[il * R + a], tile[il * R + b], sacc);
+        acc[k] = sacc;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int e = threadIdx.x + k * blockDim.x;
+    if (e < RR) t.gram[e] = acc[k];
+  }
+  if (t.pub.gamma != nullptr) {
+    __threadfence();
+    __syncthreads();
+    gamma_publish_body(t.pub, R, t.scratch, t.scratch + RR);
+  }
+}
+
 // ------------------------------------------------------------ MU / HALS ----
 // One warp per row; lane l holds columns l and l+32 (R <= 64).
 constexpr int kRowWarps = 8;
@@ -128,7 +250,8 @@ constexpr int kRowWarps = 8;
 // Per-CTA column sums of squares (+ beta) -> partials, last CTA reduces in order.
 template <int NH>
 __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, double* red /* [nw][64] */,
-                                double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket) {
+                                double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket,
+                                const TailArgs* tail = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 #pragma unroll
   for (int q = 0; q < NH; ++q) red[warp * 64 + lane + 32 * q] = sq[q];
@@ -155,6 +278,12 @@ __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, doub
       } else if (beta) {
         beta[0] = colbuf[e];
       }
+    }
+    if (tail != nullptr && tail->hhat != nullptr) {
+      // every CTA's rows are written (last ticket); red (>= 4 * 64 doubles) holds the scales
+      __threadfence();
+      __syncthreads();
+      fused_tail(*tail, R, colbuf, red);
     }
   }
 }

@@ -140,7 +140,7 @@ static __device__ void warp_jacobi_eigen(double* A, double* V, int R) {
 __global__ void __launch_bounds__(kRowWarps * 32)
     ucp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
                int64_t rows, double* __restrict__ hhat, double* __restrict__ part, double* nsq, double* beta,
-               int* status, unsigned int* ticket, int64_t mld) {
+               int* status, unsigned int* ticket, int64_t mld, TailArgs tail) {
   extern __shared__ double dsm[];
   double* L = dsm;                       // R x R (kMaxRank^2 reserved)
   double* V = dsm + kMaxRank * kMaxRank;  // eigenvectors (lstsq fallback only)
@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
       }
     }
   }
-  colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket);
+  tail.scratch = L;   // the factorisation is dead after the rows
+  colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail);
 }
 
 // ----------------------------------------------------------------- ADMM ----
@@ -489,14 +490,15 @@ int row_blocks(int64_t rows);
 static int grid_rows(int64_t rows) { return row_blocks(rows); }
 
 int ucp(const double* grams, int order, int mode, int rank, const double* mrows, int64_t rows, double* hhat,
-        double* nsq, double* beta, int* status, void* ws, size_t ws_bytes, cudaStream_t st, int64_t mld) {
+        double* nsq, double* beta, int* status, void* ws, size_t ws_bytes, cudaStream_t st, int64_t mld,
+        const TailArgs* tail) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int blocks = grid_rows(rows);
   if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (ucp)");
   constexpr int smem = int(sizeof(double)) * (2 * kMaxRank * kMaxRank + kRowWarps * kMaxRank);
   if (int rc = set_max_smem_once<ucp_kernel>(smem)) return rc;
   ucp_kernel<<<blocks, kRowWarps * 32, smem, st>>>(grams, order, mode, rank, mrows, rows, hhat, w.part, nsq, beta,
-                                                   status, w.tickets + T_UPDATE, mld);
+                                                   status, w.tickets + T_UPDATE, mld, tail ? *tail : TailArgs{});
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

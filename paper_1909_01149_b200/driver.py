@@ -266,6 +266,11 @@ class _EventTimer:
 # ------------------------------------------------------------ engine --------
 
 SLICED_MIN_ELEMS = 1 << 22       # below this the fp64 path's fewer launches win
+# rows * R^2 up to which the update kernel's last CTA also normalises and forms the Gram
+# (nncp_update_normalize).  Measured: 64^3 R=10 (6.4e3) 0.0904 -> 0.0887 ms/iter; at
+# 512^3 R=16 (1.3e5) one CTA doing the Gram is already slower than the separate
+# normalise launch (0.412 -> 0.466 ms/iter), at 1024^3 R=32 (1.0e6) far slower.
+FUSED_TAIL_MAX = 1 << 14
 SLICED_HBM_MARGIN = 4 << 30      # bytes left free after the slices
 # partial-MTTKRP cost model for mttkrp_kernel="auto" (B200 measurements):
 # FP64 DMMA path reaches ~87% of max(8 I / BW, 2 I R / 37.1 TF); the sliced path streams
@@ -607,6 +612,21 @@ class _Engine:
             m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
             self._cmark("ReduceScatter")
             last = n == N - 1
+            rows_n = self.n_owned[n]
+            if in_place and R <= 32 and 1 <= rows_n and rows_n * R * R <= FUSED_TAIL_MAX:
+                # small single-context block: the update kernel's last CTA also normalises,
+                # forms the Gram (and for the last mode gamma + the status hand-off)
+                _lib.check(lib.nncp_update_normalize(
+                    self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned), _lib.ptr(self.owned[n]),
+                    _lib.ptr(self.lam), rows_n, _lib.ptr(self.hhat), _lib.ptr(self.nsq),
+                    _lib.ptr(self.xvec) if last else None, _lib.ptr(self.status[n]), 1e-16,
+                    _lib.ptr(self.bpp_sets[n]) if self.bpp_sets else None, m_ld, _lib.ptr(self.grams[n]),
+                    _lib.vp(self.scal.data_ptr() + 8) if last else None, _lib.ptr(self.status), N,
+                    _lib.vp(self.xvec.data_ptr() + 8), self.nranks * N, self.me * N, _lib.ptr(self.masks),
+                    self.ws.ptr, self.ws.nbytes, st))
+                self.timer.mark("NNLS")
+                published = published or last
+                continue
             if cfg.algorithm in FUSED_ALGORITHMS:
                 _lib.check(lib.nncp_update_ex(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
                                               _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
