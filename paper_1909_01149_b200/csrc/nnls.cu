@@ -61,10 +61,15 @@ __global__ void __launch_bounds__(kRowWarps * 32)
         h[q] = (r < R) ? h[q] * m[q] / (d[q] + mu_eps) : 0.0;
       }
     } else {
-      // updaters.py:107-118: Gauss-Seidel over columns with the latest values
+      // updaters.py:107-118: Gauss-Seidel over columns with the latest values.  The
+      // division by S_rr sat on the sequential column chain (~15% of the kernel):
+      // its reciprocal is formed while the dot product reduces, and the quotient is
+      // the reciprocal product plus one FMA residual correction (the correctly
+      // rounded x / S_rr in all but rare tie cases).
       for (int r = 0; r < R; ++r) {
         const double dg = S[r * R + r];
         if (dg <= 0.0) continue;
+        const double idg = 1.0 / dg;
         double p = 0.0;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -74,7 +79,10 @@ __global__ void __launch_bounds__(kRowWarps * 32)
         const double dot = warp_sum(p);
         if ((r & 31) == lane) {
           const int q = r >> 5;
-          const double col = (q ? h[1] : h[0]) + ((q ? m[1] : m[0]) - dot) / dg;
+          const double num = (q ? m[1] : m[0]) - dot;
+          const double q0 = num * idg;
+          const double quo = fma(fma(-q0, dg, num), idg, q0);
+          const double col = (q ? h[1] : h[0]) + quo;
           const double v = (col < 0.0) ? 0.0 : col;
           if (q) h[1] = v; else h[0] = v;
         }

@@ -12,18 +12,27 @@ namespace nncp {
 // lane-consecutive addresses, no 32-way shared-memory bank conflict at R = 32.
 template <bool TRANSPOSED = false>
 static __device__ void load_hadamard(double* S, const double* __restrict__ grams, int order, int mode, int R) {
+  // every load of an element's 2 (order - 1) Gram entries is issued before the
+  // products (one L2 round trip per element instead of one per Gram: the per-CTA
+  // prologue was ~25% of a small update kernel)
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int a = e / R, b = e - (e / R) * R;
     double v;
     if (order == 0) {
       v = grams[e];
     } else {
-      v = 1.0;
-      for (int m = 0; m < order; ++m) {
-        if (m == mode) continue;
+      double x[kMaxOrder], y[kMaxOrder];
+#pragma unroll
+      for (int m = 0; m < kMaxOrder; ++m) {
+        const bool use = m < order && m != mode;
         const double* g = grams + size_t(m) * R * R;
-        v *= 0.5 * (g[a * R + b] + g[b * R + a]);
+        x[m] = use ? __ldg(g + a * R + b) : 0.0;
+        y[m] = use ? __ldg(g + b * R + a) : 0.0;
       }
+      v = 1.0;
+#pragma unroll
+      for (int m = 0; m < kMaxOrder; ++m)
+        if (m < order && m != mode) v *= 0.5 * (x[m] + y[m]);
     }
     S[TRANSPOSED ? b * R + a : e] = v;
   }
