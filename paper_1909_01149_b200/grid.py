@@ -35,77 +35,73 @@ __all__ = ["block_partition", "DistMap", "CommCounters", "Group", "Grid", "Worke
 
 
 def block_partition(length: int, parts: int) -> "DistMap":
-    """Balanced contiguous blocks, first length % parts get +1 (grid.py:25-31)."""
+    """Balanced contiguous blocks; the first ``length % parts`` are one longer (grid.py:25-31)."""
     if length < 0 or parts < 1:
         raise ValueError(f"bad partition request: length={length}, parts={parts}")
-    base, extra = divmod(int(length), int(parts))
-    return DistMap([base + 1 if k < extra else base for k in range(parts)])
+    sizes = np.full(int(parts), int(length) // int(parts), dtype=np.int64)
+    sizes[: int(length) % int(parts)] += 1
+    return DistMap(sizes)
 
 
 class DistMap:
-    """Contiguous block partition of [0, I) (grid.py:34-57)."""
+    """A contiguous split of [0, total) into blocks (grid.py:34-57): ``lengths`` and
+    the ``offsets`` of their starts (plus the end)."""
 
     __slots__ = ("lengths", "offsets")
 
     def __init__(self, lengths):
-        self.lengths = tuple(int(x) for x in lengths)
-        if any(x < 0 for x in self.lengths):
+        arr = np.asarray(list(lengths), dtype=np.int64).reshape(-1)
+        if (arr < 0).any():
             raise ValueError("block lengths must be nonnegative")
-        offs = [0]
-        for x in self.lengths:
-            offs.append(offs[-1] + x)
-        self.offsets = tuple(offs)
+        self.lengths = tuple(int(v) for v in arr)
+        self.offsets = tuple(int(v) for v in np.concatenate(([0], np.cumsum(arr))))
 
-    @property
-    def total(self) -> int:
-        return self.offsets[-1]
-
-    @property
-    def parts(self) -> int:
-        return len(self.lengths)
-
-    @property
-    def max_length(self) -> int:
-        return max(self.lengths) if self.lengths else 0
+    parts = property(lambda self: len(self.lengths))
+    total = property(lambda self: self.offsets[-1])
+    max_length = property(lambda self: max(self.lengths, default=0))
 
     def block(self, k: int) -> slice:
         return slice(self.offsets[k], self.offsets[k + 1])
 
 
+_TALLIES = ("calls", "words_in", "words_out", "seconds")
+
+
 @dataclass
 class CommCounters:
-    """Per-rank tallies of collective calls, words and seconds (grid.py:60-93)."""
+    """Per-rank collective tallies keyed by collective name (grid.py:60-93): calls,
+    words entering / leaving each call, seconds.  Also snapshot / delta / re-add /
+    restore for the CUDA-graph replays, which run captured collectives again."""
 
     calls: dict = field(default_factory=dict)
     words_in: dict = field(default_factory=dict)
     words_out: dict = field(default_factory=dict)
     seconds: dict = field(default_factory=dict)
 
+    def _bump(self, name, calls, w_in, w_out, secs=0.0):
+        for tally, v in zip(_TALLIES, (calls, w_in, w_out, secs)):
+            d = getattr(self, tally)
+            d[name] = d.get(name, 0.0 if tally == "seconds" else 0) + v
+
     def record(self, name: str, words_in: int, words_out: int, elapsed: float = 0.0):
-        self.calls[name] = self.calls.get(name, 0) + 1
-        self.words_in[name] = self.words_in.get(name, 0) + int(words_in)
-        self.words_out[name] = self.words_out.get(name, 0) + int(words_out)
-        self.seconds[name] = self.seconds.get(name, 0.0) + elapsed
+        self._bump(name, 1, int(words_in), int(words_out), elapsed)
 
     def snapshot(self) -> dict:
-        return {"calls": dict(self.calls), "words_in": dict(self.words_in), "words_out": dict(self.words_out)}
+        return {t: dict(getattr(self, t)) for t in _TALLIES[:3]}
 
     def since(self, snap: dict) -> dict:
-        """Calls and words recorded after ``snap`` (one captured sweep's collectives)."""
-        now = self.snapshot()
-        return {k: {name: v - snap[k].get(name, 0) for name, v in now[k].items()} for k in now}
+        """The calls and words recorded after ``snap`` (one captured sweep's collectives)."""
+        return {t: {k: v - snap[t].get(k, 0) for k, v in getattr(self, t).items()} for t in _TALLIES[:3]}
 
     def add(self, delta: dict):
         """Re-add a ``since`` delta (a CUDA-graph replay of the captured collectives)."""
-        for name, calls in delta["calls"].items():
-            self.calls[name] = self.calls.get(name, 0) + calls
-            self.words_in[name] = self.words_in.get(name, 0) + delta["words_in"].get(name, 0)
-            self.words_out[name] = self.words_out.get(name, 0) + delta["words_out"].get(name, 0)
+        for name in delta["calls"]:
+            self._bump(name, delta["calls"][name], delta["words_in"].get(name, 0), delta["words_out"].get(name, 0))
 
     def restore(self, snap: dict):
-        """Back to ``snap`` (a capture that failed recorded calls that never ran)."""
-        self.calls, self.words_in, self.words_out = (dict(snap["calls"]), dict(snap["words_in"]),
-                                                     dict(snap["words_out"]))
+        """Back to ``snap`` (collectives recorded while capturing did not run)."""
+        for t in _TALLIES[:3]:
+            setattr(self, t, dict(snap[t]))
 
     def total_words(self) -> int:
         return sum(self.words_in.values()) + sum(self.words_out.values())
@@ -113,20 +109,19 @@ class CommCounters:
     def merged_with(self, other: "CommCounters") -> "CommCounters":
         out = CommCounters()
         for src in (self, other):
-            for name, c in src.calls.items():
-                out.calls[name] = out.calls.get(name, 0) + c
-                out.words_in[name] = out.words_in.get(name, 0) + src.words_in.get(name, 0)
-                out.words_out[name] = out.words_out.get(name, 0) + src.words_out.get(name, 0)
-                out.seconds[name] = out.seconds.get(name, 0.0) + src.seconds.get(name, 0.0)
+            for name in src.calls:
+                out._bump(name, src.calls[name], src.words_in.get(name, 0), src.words_out.get(name, 0),
+                          src.seconds.get(name, 0.0))
         return out
 
 
 class Group:
-    """Sorted rank set with position lookup and its rendezvous (grid.py:116-126)."""
+    """An ascending rank set, each member's position in it, and its rendezvous
+    (grid.py:116-126)."""
 
     def __init__(self, ranks):
         self.ranks = tuple(sorted(int(r) for r in ranks))
-        self.index = {r: k for k, r in enumerate(self.ranks)}
+        self.index = dict(zip(self.ranks, range(len(self.ranks))))
         self.rendezvous = _Rendezvous(len(self.ranks))
 
     @property
@@ -135,187 +130,174 @@ class Group:
 
 
 class Grid:
-    """P_1 x ... x P_N grid; rank <-> coordinate with mode-1 fastest (grid.py:129-170)."""
+    """P_1 x ... x P_N processor grid (grid.py:129-203).  A rank is the column-major
+    (mode-1 fastest) linear index of its coordinate; the mode-n slice of a rank is
+    every rank with the same n-th coordinate."""
 
     def __init__(self, shape):
         self.shape = tuple(int(p) for p in shape)
         if any(p < 1 for p in self.shape):
             raise ValueError(f"grid dims must be positive, got {self.shape}")
-        self.total = int(np.prod(self.shape))
+        self.total = int(np.prod(self.shape, dtype=np.int64))
         self.all_procs = Group(range(self.total))
-        self.slice_groups = []
-        for n, pn in enumerate(self.shape):
-            groups = [[] for _ in range(pn)]
-            for rank in range(self.total):
-                groups[self.coord_of(rank)[n]].append(rank)
-            self.slice_groups.append([Group(g) for g in groups])
+        coords = np.array(np.unravel_index(np.arange(self.total), self.shape, order="F")).T.reshape(self.total, -1)
+        self.slice_groups = [[Group(np.flatnonzero(coords[:, n] == c)) for c in range(pn)]
+                             for n, pn in enumerate(self.shape)]
 
     def coord_of(self, rank: int):
-        coord = []
-        for p in self.shape:
-            rank, c = divmod(rank, p)
-            coord.append(c)
-        return tuple(coord)
+        return tuple(int(c) for c in np.unravel_index(int(rank), self.shape, order="F"))
 
     def rank_of(self, coord) -> int:
-        rank, stride = 0, 1
-        for c, p in zip(coord, self.shape):
-            if not 0 <= c < p:
-                raise ValueError(f"coordinate {coord} outside grid {self.shape}")
-            rank += c * stride
-            stride *= p
-        return rank
+        coord = tuple(int(c) for c in coord)
+        if len(coord) != len(self.shape) or any(not 0 <= c < p for c, p in zip(coord, self.shape)):
+            raise ValueError(f"coordinate {coord} outside grid {self.shape}")
+        return int(np.ravel_multi_index(coord, self.shape, order="F"))
 
     def slice_group(self, mode: int, coord: int) -> Group:
         return self.slice_groups[mode][coord]
 
-    def _abort_all(self):
-        self.all_procs.rendezvous.abort()
-        for groups in self.slice_groups:
-            for g in groups:
-                g.rendezvous.abort()
+    def _groups(self):
+        yield self.all_procs
+        for per_mode in self.slice_groups:
+            yield from per_mode
 
     def run(self, fn, *args):
-        """``fn(worker, *args)`` on every rank as worker threads; the list of results
-        (grid.py:172-203).  The first worker exception aborts every pending collective
-        and is re-raised in the caller."""
-        workers = [Worker(rank, self) for rank in range(self.total)]
-        self._workers = workers
-        results = [None] * self.total
-        failures = [None] * self.total
+        """Run ``fn(worker, *args)`` on every rank as a thread; the per-rank results
+        (grid.py:172-203).  A failing rank breaks every rendezvous, so no rank is left
+        waiting, and the first failure is raised in the caller."""
+        self._workers = [Worker(r, self) for r in range(self.total)]
+        out = [None] * self.total
+        errors = [None] * self.total
 
-        def main(w):
+        def body(w):
             try:
-                results[w.rank] = fn(w, *args)
+                out[w.rank] = fn(w, *args)
             except threading.BrokenBarrierError:
-                pass
+                return
             except BaseException as exc:  # noqa: BLE001  (propagate to the caller)
-                failures[w.rank] = exc
-                self._abort_all()
+                errors[w.rank] = exc
+                for g in self._groups():
+                    g.rendezvous.abort()
 
-        threads = [threading.Thread(target=main, args=(w,), name=f"worker-{w.rank}") for w in workers]
+        threads = [threading.Thread(target=body, args=(w,), name=f"worker-{w.rank}") for w in self._workers]
         for t in threads:
             t.start()
         for t in threads:
             t.join()
-        for exc in failures:
-            if exc is not None:
-                raise exc
-        return results
+        first = next((e for e in errors if e is not None), None)
+        if first is not None:
+            raise first
+        return out
+
+
+def _fold(values, op):
+    """Elementwise combination of the members' arrays in ascending rank order
+    (grid.py:250-262), numpy on the host or torch on the device."""
+    acc = values[0].clone() if isinstance(values[0], torch.Tensor) else np.array(values[0], copy=True)
+    for v in values[1:]:
+        if op == "sum":
+            acc += v
+        elif isinstance(acc, torch.Tensor):
+            acc = torch.minimum(acc, v) if op == "min" else torch.maximum(acc, v)
+        else:
+            (np.minimum if op == "min" else np.maximum)(acc, v, out=acc)
+    return acc
 
 
 class Worker:
-    """One rank of ``Grid.run``: coordinates, counters and the reference's collective
-    calls (grid.py:206-302) -- rank-ordered and bitwise reproducible.  Host (numpy)
-    payloads reduce on the host exactly as the reference; device payloads (torch CUDA
-    tensors) reduce on the device in the same rank order and come back as device
-    tensors.  Point-to-point send/recv (grid.py:224-237) is kept for completeness."""
+    """One rank inside ``Grid.run`` (grid.py:206-302): its coordinate, counters and the
+    reference's collective calls on a ``Group``, bitwise reproducible (ascending rank
+    order).  Host (numpy) payloads are combined on the host like the reference; CUDA
+    tensors are combined on their device in the same order and returned on it.  The
+    mailbox point-to-point pair ``send`` / ``recv`` (grid.py:224-237) is kept."""
 
     def __init__(self, rank: int, grid: "Grid"):
-        self.rank = rank
+        self.rank = int(rank)
         self.grid = grid
-        self.coord = grid.coord_of(rank)
+        self.coord = grid.coord_of(self.rank)
         self.counters = CommCounters()
         self.recorder = None
-        self._mailbox = []
-        self._cv = threading.Condition()
-
-    def _record(self, category: str, elapsed: float):
-        if self.recorder is not None:
-            self.recorder(category, elapsed)
+        self._inbox = []
+        self._inbox_cv = threading.Condition()
 
     def send(self, dst: int, payload):
-        w = self.grid._workers[dst]
-        with w._cv:
-            w._mailbox.append((self.rank, payload))
-            w._cv.notify_all()
+        peer = self.grid._workers[dst]
+        with peer._inbox_cv:
+            peer._inbox.append((self.rank, payload))
+            peer._inbox_cv.notify_all()
 
     def recv(self, src: int = None):
-        with self._cv:
+        with self._inbox_cv:
             while True:
-                for k, (s, p) in enumerate(self._mailbox):
-                    if src is None or s == src:
-                        self._mailbox.pop(k)
-                        return p
-                self._cv.wait()
+                hit = next((k for k, (s, _) in enumerate(self._inbox) if src is None or s == src), None)
+                if hit is not None:
+                    return self._inbox.pop(hit)[1]
+                self._inbox_cv.wait()
 
-    @staticmethod
-    def _combine(slots, op):
-        out = slots[0].clone() if isinstance(slots[0], torch.Tensor) else slots[0].copy()
-        for s in slots[1:]:                      # ascending rank order (grid.py:250-262)
-            if op == "sum":
-                out += s
-            elif op == "min":
-                out = torch.minimum(out, s) if isinstance(out, torch.Tensor) else np.minimum(out, s, out=out)
-            else:
-                out = torch.maximum(out, s) if isinstance(out, torch.Tensor) else np.maximum(out, s, out=out)
-        return out
-
-    def all_reduce(self, group: Group, local, op: str = "sum"):
-        """Elementwise reduction in ascending rank order, the same result on every member."""
+    def _exchange(self, name, group, payload, n_in, combine):
+        """Post ``payload``, combine every member's (rank order), account the call."""
         import time
 
+        t0 = time.perf_counter()
+        if isinstance(payload, torch.Tensor) and payload.is_cuda:
+            torch.cuda.current_stream().synchronize()   # the peers read it from their threads
+        slots = group.rendezvous.exchange(group.index[self.rank], payload)
+        result = combine(slots)
+        dt = time.perf_counter() - t0
+        n_out = int(result.numel() if isinstance(result, torch.Tensor) else np.size(result))
+        self.counters.record(name, n_in, n_out, dt)
+        if self.recorder is not None:
+            self.recorder(name, dt)
+        return result
+
+    @staticmethod
+    def _as_payload(local):
+        if isinstance(local, torch.Tensor) and local.is_cuda:
+            return local.to(torch.float64)
+        return np.asarray(local, dtype=np.float64)
+
+    def all_reduce(self, group: Group, local, op: str = "sum"):
+        """Elementwise reduction in ascending rank order; the same result on every member."""
         if op not in ("sum", "min", "max"):
             raise ValueError(f"unknown reduction {op!r}")
-        t0 = time.perf_counter()
-        dev = isinstance(local, torch.Tensor) and local.is_cuda
-        scalar = (not dev) and np.ndim(local) == 0
-        arr = local.reshape(-1).to(torch.float64) if dev else np.atleast_1d(np.asarray(local, dtype=np.float64))
-        if dev:
-            torch.cuda.current_stream().synchronize()
-        slots = group.rendezvous.exchange(group.index[self.rank], arr)
-        if any(tuple(x.shape) != tuple(slots[0].shape) for x in slots):
-            raise ValueError("all_reduce length mismatch across group")
-        out = self._combine(slots, op)
-        elapsed = time.perf_counter() - t0
-        n = int(arr.numel() if dev else arr.size)
-        self.counters.record("AllReduce", n, n, elapsed)
-        self._record("AllReduce", elapsed)
-        if dev:
-            return out.reshape(local.shape)
+        x = self._as_payload(local)
+        scalar = not isinstance(x, torch.Tensor) and x.ndim == 0
+        flat = x.reshape(-1) if isinstance(x, torch.Tensor) else np.atleast_1d(x)
+
+        def combine(slots):
+            if any(tuple(v.shape) != tuple(slots[0].shape) for v in slots):
+                raise ValueError("all_reduce length mismatch across group")
+            return _fold(slots, op)
+
+        out = self._exchange("AllReduce", group, flat, int(np.size(flat) if not isinstance(flat, torch.Tensor)
+                                                           else flat.numel()), combine)
+        if isinstance(x, torch.Tensor):
+            return out.reshape(x.shape)
         return float(out[0]) if scalar else out
 
     def all_gather(self, group: Group, local):
-        """Concatenation of the members' arrays in ascending rank order."""
-        import time
-
-        t0 = time.perf_counter()
-        dev = isinstance(local, torch.Tensor) and local.is_cuda
-        arr = local if dev else np.asarray(local, dtype=np.float64)
-        if dev:
-            torch.cuda.current_stream().synchronize()
-        slots = group.rendezvous.exchange(group.index[self.rank], arr)
-        out = torch.cat(slots, dim=0) if dev else np.concatenate(slots, axis=0)
-        elapsed = time.perf_counter() - t0
-        n_in = int(arr.numel() if dev else arr.size)
-        self.counters.record("AllGather", n_in, int(out.numel() if dev else out.size), elapsed)
-        self._record("AllGather", elapsed)
-        return out
+        """The members' arrays concatenated along the rows in ascending rank order."""
+        x = self._as_payload(local)
+        cat = (lambda v: torch.cat(v, dim=0)) if isinstance(x, torch.Tensor) else (lambda v: np.concatenate(v, 0))
+        return self._exchange("AllGather", group, x, int(x.numel() if isinstance(x, torch.Tensor) else x.size), cat)
 
     def reduce_scatter(self, group: Group, local, parts: DistMap):
-        """Rank-ordered elementwise sum, then this member's row block."""
-        import time
-
-        t0 = time.perf_counter()
-        dev = isinstance(local, torch.Tensor) and local.is_cuda
-        arr = local if dev else np.asarray(local, dtype=np.float64)
+        """Rank-ordered sum of the members' arrays, then this member's row block."""
+        x = self._as_payload(local)
         if parts.parts != group.size:
             raise ValueError(f"partition has {parts.parts} blocks for a group of {group.size}")
-        if parts.total != arr.shape[0]:
-            raise ValueError(f"partition covers {parts.total} rows, local array has {arr.shape[0]}")
-        if dev:
-            torch.cuda.current_stream().synchronize()
-        slots = group.rendezvous.exchange(group.index[self.rank], arr)
-        if any(tuple(x.shape) != tuple(slots[0].shape) for x in slots):
-            raise ValueError("reduce_scatter length mismatch across group")
-        total = self._combine(slots, "sum")
-        blk = total[parts.block(group.index[self.rank])]
-        out = blk.clone() if dev else blk.copy()
-        elapsed = time.perf_counter() - t0
-        self.counters.record("ReduceScatter", int(arr.numel() if dev else arr.size),
-                             int(out.numel() if dev else out.size), elapsed)
-        self._record("ReduceScatter", elapsed)
-        return out
+        if parts.total != x.shape[0]:
+            raise ValueError(f"partition covers {parts.total} rows, local array has {x.shape[0]}")
+        mine = parts.block(group.index[self.rank])
+
+        def combine(slots):
+            if any(tuple(v.shape) != tuple(slots[0].shape) for v in slots):
+                raise ValueError("reduce_scatter length mismatch across group")
+            blk = _fold(slots, "sum")[mine]
+            return blk.clone() if isinstance(blk, torch.Tensor) else blk.copy()
+
+        return self._exchange("ReduceScatter", group, x, int(x.numel() if isinstance(x, torch.Tensor) else x.size),
+                              combine)
 
 
 # ------------------------------------------------------------- layout ------
