@@ -23,9 +23,14 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
-  // HALS walks column r of S across the lanes: keep S^T (St[r][c] = S[c][r])
-  load_hadamard<ALGO == NNCP_ALGO_HALS>(S, grams, order, mode, R);
+#ifdef NNCP_UPD_TIMING
+  const long long tu0 = clock64();
+#endif
+  load_hadamard(S, grams, order, mode, R);
   __syncthreads();
+#ifdef NNCP_UPD_TIMING
+  const long long tu1 = clock64();
+#endif
   if (ALGO == NNCP_ALGO_HALS && blockIdx.x == 0) {
     for (int r = threadIdx.x; r < R; r += blockDim.x)
       if (S[r * R + r] <= 0.0) atomicOr(status + (r >> 5), int(1u << (r & 31)));
@@ -61,30 +66,45 @@ __global__ void __launch_bounds__(kRowWarps * 32)
         h[q] = (r < R) ? h[q] * m[q] / (d[q] + mu_eps) : 0.0;
       }
     } else {
-      // updaters.py:107-118: Gauss-Seidel over columns with the latest values.  The
-      // division by S_rr sat on the sequential column chain (~15% of the kernel):
-      // its reciprocal is formed while the dot product reduces, and the quotient is
-      // the reciprocal product plus one FMA residual correction (the correctly
-      // rounded x / S_rr in all but rare tie cases).
+      // updaters.py:107-118: Gauss-Seidel over columns with the latest values,
+      // h_r <- max(0, h_r + (m_r - (h S)_r) / S_rr).  Instead of a fresh warp-reduced
+      // dot product per column (a 5-level shuffle tree on the sequential column
+      // chain), every lane keeps g = h S for its columns and adds delta_r S[r, :] when
+      // h_r changes: per column one broadcast and one FMA.  The quotient is the
+      // reciprocal product plus one FMA residual correction (the correctly rounded
+      // division in all but rare tie cases), the reciprocal formed off the chain.
+      double g[2] = {0.0, 0.0};
+      for (int j = 0; j < R; ++j) {
+        const double hj = __shfl_sync(0xffffffffu, j < 32 ? h[0] : h[1], j & 31);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = lane + 32 * q;
+          if (c < R) g[q] = fma(hj, S[j * R + c], g[q]);    // (h S)[c] = sum_j h_j S[j][c]
+        }
+      }
       for (int r = 0; r < R; ++r) {
         const double dg = S[r * R + r];
         if (dg <= 0.0) continue;
         const double idg = 1.0 / dg;
-        double p = 0.0;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int cc = lane + 32 * q;
-          if (cc < R) p = fma(h[q], S[r * R + cc], p);   // S^T[r][cc] = S[cc][r]
-        }
-        const double dot = warp_sum(p);
+        const int q = r >> 5;
+        double delta = 0.0;
         if ((r & 31) == lane) {
-          const int q = r >> 5;
-          const double num = (q ? m[1] : m[0]) - dot;
+          const double num = (q ? m[1] : m[0]) - (q ? g[1] : g[0]);
           const double q0 = num * idg;
           const double quo = fma(fma(-q0, dg, num), idg, q0);
-          const double col = (q ? h[1] : h[0]) + quo;
+          const double hr0 = q ? h[1] : h[0];
+          const double col = hr0 + quo;
           const double v = (col < 0.0) ? 0.0 : col;
+          delta = v - hr0;
           if (q) h[1] = v; else h[0] = v;
+        }
+        delta = __shfl_sync(0xffffffffu, delta, r & 31);
+        if (delta != 0.0) {
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq) {
+            const int c = lane + 32 * qq;
+            if (c < R) g[qq] = fma(delta, S[r * R + c], g[qq]);
+          }
         }
       }
     }
@@ -100,7 +120,15 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     }
   }
   tail.scratch = S;   // S is dead after the rows
+#ifdef NNCP_UPD_TIMING
+  const long long tu2 = clock64();
+#endif
   colsum_epilogue<2>(sq, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail);
+#ifdef NNCP_UPD_TIMING
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("update cta %d/%d: hadamard %lld rows %lld epilogue %lld (start %lld)\n", blockIdx.x, gridDim.x, tu1 - tu0,
+           tu2 - tu1, clock64() - tu2, tu0 % 1000000);
+#endif
 }
 
 // ------------------------------------------------------------------ BPP ----
