@@ -93,3 +93,34 @@ def test_generate_synthetic_truth_matches_reference(golden):
     assert np.linalg.norm(got - g["x"]) <= 1e-14 * np.linalg.norm(g["x"])
     with pytest.raises(ValueError):
         generate_synthetic(SyntheticSpec((1024, 1024, 256), 2))
+
+
+@pytest.mark.gpu
+def test_parallel_from_file_path_and_device_tensor(tmp_path, golden):
+    """nncp_parallel takes a tensor-file path (each rank reads only its block) or a
+    device-resident DenseTensor (blocks sliced in HBM): same run as from host memory."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import warnings
+
+    import paper_1909_01149_b200 as P
+    from paper_1909_01149_b200.tensor_io import write_tensor
+
+    g = golden("runs.npz")
+    dims = tuple(int(d) for d in g["hals_odd_dims"])
+    r, iters, iseed = (int(v) for v in g["hals_odd_meta"])
+    x = P.DenseTensor(dims, g["hals_odd_x"])
+    path = str(tmp_path / "x.nncp")
+    write_tensor(path, x)
+    cfg = dict(rank=r, algorithm="hals", max_iters=iters, tol=0.0, seed=iseed, grid=(2, 2, 1))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        host = P.nncp_parallel(x, P.RunConfig(**cfg))
+        from_file = P.nncp_parallel(path, P.RunConfig(**cfg))
+        from_dev = P.nncp_parallel(x.to_device(), P.RunConfig(**cfg))
+    assert host.errors == from_file.errors == from_dev.errors
+    for a, b, c in zip(host.model.factors, from_file.model.factors, from_dev.model.factors):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert np.max(np.abs(np.array(host.errors) - g["grid_hals_odd_2x2x1_errors"])) <= 1e-9
