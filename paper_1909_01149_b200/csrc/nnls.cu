@@ -69,41 +69,46 @@ __global__ void __launch_bounds__(kRowWarps * 32)
       // updaters.py:107-118: Gauss-Seidel over columns with the latest values,
       // h_r <- max(0, h_r + (m_r - (h S)_r) / S_rr).  Instead of a fresh warp-reduced
       // dot product per column (a 5-level shuffle tree on the sequential column
-      // chain), every lane keeps g = h S for its columns and adds delta_r S[r, :] when
-      // h_r changes: per column one broadcast and one FMA.  The quotient is the
-      // reciprocal product plus one FMA residual correction (the correctly rounded
-      // division in all but rare tie cases), the reciprocal formed off the chain.
+      // chain), every lane keeps g_c = (h S)_c for its columns c, split the way the
+      // reference's dot product sees h at column c: the old values of columns j >= c
+      // (summed up front) plus the new values of columns j < c (added as each column
+      // finishes: one broadcast and one FMA).  Never old-minus-new deltas: when a
+      // column is wiped out its O(1) old value must leave g exactly, or the rounding
+      // of the cancellation lands on the tiny survivors (tensors far below the initial
+      // factors' scale).  The quotient is the reciprocal product plus one FMA residual
+      // correction (the correctly rounded division in all but rare tie cases), the
+      // reciprocal formed off the chain.
       double g[2] = {0.0, 0.0};
       for (int j = 0; j < R; ++j) {
         const double hj = __shfl_sync(0xffffffffu, j < 32 ? h[0] : h[1], j & 31);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int c = lane + 32 * q;
-          if (c < R) g[q] = fma(hj, S[j * R + c], g[q]);    // (h S)[c] = sum_j h_j S[j][c]
+          if (c < R && j >= c) g[q] = fma(hj, S[j * R + c], g[q]);    // sum_{j >= c} h_j S[j][c]
         }
       }
       for (int r = 0; r < R; ++r) {
         const double dg = S[r * R + r];
-        if (dg <= 0.0) continue;
         const double idg = 1.0 / dg;
         const int q = r >> 5;
-        double delta = 0.0;
+        double v = 0.0;
         if ((r & 31) == lane) {
-          const double num = (q ? m[1] : m[0]) - (q ? g[1] : g[0]);
-          const double q0 = num * idg;
-          const double quo = fma(fma(-q0, dg, num), idg, q0);
-          const double hr0 = q ? h[1] : h[0];
-          const double col = hr0 + quo;
-          const double v = (col < 0.0) ? 0.0 : col;
-          delta = v - hr0;
-          if (q) h[1] = v; else h[0] = v;
+          v = q ? h[1] : h[0];   // a skipped column (S_rr <= 0) keeps its value
+          if (dg > 0.0) {
+            const double num = (q ? m[1] : m[0]) - (q ? g[1] : g[0]);
+            const double q0 = num * idg;
+            const double quo = fma(fma(-q0, dg, num), idg, q0);
+            const double col = v + quo;
+            v = (col < 0.0) ? 0.0 : col;
+            if (q) h[1] = v; else h[0] = v;
+          }
         }
-        delta = __shfl_sync(0xffffffffu, delta, r & 31);
-        if (delta != 0.0) {
+        v = __shfl_sync(0xffffffffu, v, r & 31);
+        if (v != 0.0) {
 #pragma unroll
           for (int qq = 0; qq < 2; ++qq) {
             const int c = lane + 32 * qq;
-            if (c < R) g[qq] = fma(delta, S[r * R + c], g[qq]);
+            if (c < R && c > r) g[qq] = fma(v, S[r * R + c], g[qq]);
           }
         }
       }
@@ -398,7 +403,7 @@ __device__ bool bpp_schur(const double* TT, int R, unsigned long long P, double*
 
 // T^T = (S^-1)^T for the block-elimination passes, by Gauss-Jordan on [S | I] without
 // pivoting (S = Hadamard of Grams is symmetric positive definite when nonsingular: the
-// pivots are Schur complements).  Block-cooperative, two barriers per step; returns
+// pivots are Schur complements).  Block-cooperative, one barrier per step; returns
 // false (uniformly) when a pivot is not comfortably positive -- the kernel then solves
 // every pass directly.  (A Newton-Schulz refresh from the previous sweep's inverse was
 // measured slower: S moves by 1e-2..1 between sweeps early on, and each R^3 product in
@@ -407,26 +412,36 @@ template <int RP>
 __device__ bool block_inverse(const double* S, int R, double* aug, double* TT, double* gj) {
   constexpr int W = 2 * RP;   // [S | I] with row pitch 2 RP; warp w owns rows w, w + nw, ...
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* rowbuf = gj;        // 2 RP: the scaled pivot row
-  double* colfac = gj + 2 * RP;   // RP: the pivot column before the step
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
+  // the step's pivot row and column (unscaled, as the previous step left them) in
+  // double-buffered shared rows: whoever writes an element of the next pivot row or
+  // column also stores it there, so each step needs ONE block barrier
+  double* rowb[2] = {gj, gj + 2 * RP};            // 2 RP each
+  double* colb[2] = {gj + 4 * RP, gj + 5 * RP};   // RP each
   for (int i = warp; i < R; i += nw)
-    for (int j = lane; j < 2 * R; j += 32)
-      aug[i * W + j] = j < R ? S[j * R + i] : (j - R == i ? 1.0 : 0.0);
+    for (int j = lane; j < 2 * R; j += 32) {
+      const double v = j < R ? S[j * R + i] : (j - R == i ? 1.0 : 0.0);
+      aug[i * W + j] = v;
+      if (i == 0) rowb[0][j] = v;
+      if (j == 0) colb[0][i] = v;
+    }
   __syncthreads();
   for (int c = 0; c < R; ++c) {
-    const double piv = aug[c * W + c];
+    const double* row = rowb[c & 1];
+    const double* col = colb[c & 1];
+    double* nrow = rowb[(c + 1) & 1];
+    double* ncol = colb[(c + 1) & 1];
+    const double piv = row[c];
+    if (!(piv > 1e-8 * fabs(S[c * R + c]))) return false;   // uniform: every thread reads the same piv
     const double inv = 1.0 / piv;
-    if (threadIdx.x == 0 && !(piv > 1e-8 * fabs(S[c * R + c]))) bad = 1;
-    for (int j = threadIdx.x; j < 2 * R; j += blockDim.x) rowbuf[j] = aug[c * W + j] * inv;
-    for (int i = threadIdx.x; i < R; i += blockDim.x) colfac[i] = aug[i * W + c];
-    __syncthreads();
-    if (bad) return false;
     for (int i = warp; i < R; i += nw) {
-      const double f = colfac[i];
-      for (int j = lane; j < 2 * R; j += 32)
-        aug[i * W + j] = (i == c) ? rowbuf[j] : fma(-f, rowbuf[j], aug[i * W + j]);
+      const double f = col[i];
+      for (int j = lane; j < 2 * R; j += 32) {
+        const double pr = row[j] * inv;
+        const double v = (i == c) ? pr : fma(-f, pr, aug[i * W + j]);
+        aug[i * W + j] = v;
+        if (i == c + 1) nrow[j] = v;
+        if (j == c + 1) ncol[i] = v;
+      }
     }
     __syncthreads();
   }
@@ -451,8 +466,8 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
   double* red = TT + RP * RP;                         // NW * 64
   double* colbuf = red + NW * 64;                     // RP + 1
   double* zall = colbuf + RP + 1;                     // NW * RP
-  double* gj = zall + NW * RP;                        // 3 * RP (Gauss-Jordan row / column buffers)
-  double* fall = gj + 3 * RP;                         // NW * RP (each warp's right-hand side f)
+  double* gj = zall + NW * RP;                        // 6 * RP (Gauss-Jordan row / column buffers)
+  double* fall = gj + 6 * RP;                         // NW * RP (each warp's right-hand side f)
   double* lu = fall + NW * RP;                        // NW * RP * LP (the inverse's work space at the start)
   int* pidx_all = reinterpret_cast<int*>(lu + size_t(NW) * RP * LP);   // NW * 64
   int* qidx_all = pidx_all + NW * 64;                                  // NW * 64
@@ -865,7 +880,7 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
       constexpr int NW = bpp_warps<RP>();
       const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms())));
       if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (bpp)");
-      const size_t smem = sizeof(double) * (2 * size_t(RP) * RP + NW * 64 + RP + 1 + 2 * NW * RP + 3 * RP +
+      const size_t smem = sizeof(double) * (2 * size_t(RP) * RP + NW * 64 + RP + 1 + 2 * NW * RP + 6 * RP +
                                             size_t(NW) * RP * (RP + 1)) +
                           sizeof(int) * NW * 128;
       if (int rc = set_max_smem_once<bpp_kernel<RP>>(int(smem))) return rc;

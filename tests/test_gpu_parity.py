@@ -371,3 +371,68 @@ def test_runs_vs_oracle_tma_sizes(P, dims, r, algo, iters):
     assert np.max(np.abs(np.array(rep.errors) - np.array(errors))) <= TRACE_TOL
     for a, b in zip(rep.model.factors, factors):
         assert np.max(np.abs(a - b)) <= FACTOR_TOL
+
+
+def _gram_blocked(blk):
+    """H^T H summed in blk-row blocks in sequence: another legal order for the Gram."""
+    def gram(h):
+        g = np.zeros((h.shape[1], h.shape[1]))
+        for i in range(0, h.shape[0], blk):
+            g = g + h[i:i + blk].T @ h[i:i + blk]
+        return 0.5 * (g + g.T)
+    return gram
+
+
+@pytest.mark.parametrize("dims,rank,scale,strict,engine,sensitive", [
+    ((34, 16, 32), 16, -33, True, "fp64", False),       # round-2 fuzz (seed 2027) case 160's class
+    ((34, 16, 32), 16, -33, True, "sliced", False),
+    ((2, 906, 733), 64, -45, False, "auto", False),     # round-2 --large case 9's class, smaller
+    ((7, 1516, 129), 33, -43, False, "fp64", True),     # round-2 --large case 27's class, smaller
+])
+def test_hals_tensor_far_below_initial_factors(P, dims, rank, scale, strict, engine, sensitive):
+    """A tensor scaled by 2^-33..2^-45 against U[0,1) initial factors: the first HALS
+    update wipes out most columns and the survivors are O(1) - O(1) + tiny.  The row
+    product g = h S must see the wiped columns' old values leave exactly (the device
+    sums old values of columns >= c plus new values of columns < c, like the
+    reference's fresh dot product); an old-minus-new incremental g put 1e-9..1e-5 on
+    the first traced error.  Trace and lambda against the oracle.
+
+    ``sensitive``: inputs where the survivors also carry S's own rounding, so the
+    reference's trace moves when only its Gram is summed in another legal order (row blocks
+    of 16 / 32 / 128)
+    (tools/fuzz_gap_reference.py); there the device trace must stay within 10x that
+    spread (and lambda / factors within the usual tolerances)."""
+    rng = np.random.default_rng(0)
+    hs = [rng.random((d, rank)) for d in dims]
+    x = O.khatri_rao(hs) @ np.ones(rank)
+    x = (x + 0.05 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))) * 2.0 ** scale
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        errors, factors, lam, _, _ = O.run_sequential(x, dims, rank, "hals", 4, 0.0, 0, strict_split=strict)
+        rep = P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(rank=rank, algorithm="hals", max_iters=4, tol=0.0,
+                                                                    seed=0, strict_split=strict, mttkrp_kernel=engine))
+    e, o = np.array(rep.errors), np.array(errors)
+    trace = float(np.max(np.abs(e - o) / np.maximum(1.0, o)))
+    keep = lam > 0
+    lrel = float(np.max(np.abs(rep.model.lam[keep] - lam[keep]) / lam[keep]))
+    fac = max(float(np.max(np.abs(a - b))) for a, b in zip(rep.model.factors, factors))
+    tol = TRACE_TOL
+    if sensitive:
+        stock, spread = O.gram, 0.0
+        try:
+            for blk in (16, 32, 128):
+                O.gram = _gram_blocked(blk)
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    alt = np.array(O.run_sequential(x, dims, rank, "hals", 4, 0.0, 0, strict_split=strict)[0])
+                spread = max(spread, float(np.max(np.abs(alt - o) / np.maximum(1.0, o))))
+        finally:
+            O.gram = stock
+        assert spread > TRACE_TOL, spread     # the input really is rounding-sensitive
+        tol = 10.0 * spread
+    print(f"{dims} R={rank} x*2^{scale} {engine}: trace {trace:.1e} (tol {tol:.1e}) lambda {lrel:.1e} "
+          f"factors {fac:.1e}")
+    assert trace <= tol
+    assert np.array_equal(rep.model.lam > 0, keep)
+    assert lrel <= 1e-9
+    assert fac <= FACTOR_TOL

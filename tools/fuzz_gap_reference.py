@@ -1,7 +1,9 @@
-"""The two fuzz mismatches of round 1 (tensors scaled by 2^-57 / 2^-51 against U[0,1)
-initial factors) re-run on the UNMODIFIED reference itself: its own sequential and
-grid runs disagree by the same order, i.e. the inputs are ill-posed, not the device
-path wrong.  CPU only; needs /root/reference (or baseline/_ref).
+"""The scaled-tensor fuzz mismatches (tensors scaled by 2^-57 / 2^-51 in round 1,
+2^-33 / 2^-43 / 2^-45 in round 2's sweeps, against U[0,1) initial factors) re-run on
+the UNMODIFIED reference itself: its own sequential and grid runs disagree by the same
+order, i.e. the inputs are ill-posed (the first update cancels O(1) terms down to the
+tensor's scale), not the device path wrong.  CPU only; needs /root/reference (or
+baseline/_ref).
 
     python tools/fuzz_gap_reference.py > profiles/r02_fuzz_gap_reference.log
 """
@@ -20,7 +22,10 @@ import nncp  # noqa: E402
 
 warnings.simplefilter("ignore")
 CASES = [((4, 5, 4, 6), 40, "hals", -57, (3, 1, 2, 3), True),      # round-1 fuzz9 case 77
-         ((1347, 6, 11, 102), 64, "hals", -51, (3, 1, 1, 1), False)]  # round-1 fuzz12 case 9
+         ((1347, 6, 11, 102), 64, "hals", -51, (3, 1, 1, 1), False),  # round-1 fuzz12 case 9
+         ((34, 16, 32), 16, "hals", -33, (1, 3, 3), True),           # round-2 fuzz (seed 2027) case 160
+         ((7, 15162, 129), 33, "hals", -43, (1, 1, 3), False),       # round-2 --large (seed 2028) case 27
+         ((2, 906, 7335), 64, "hals", -45, (1, 3, 3), False)]        # round-2 --large (seed 2028) case 9
 for dims, rank, algo, scale, grid, strict in CASES:
     for seed in range(3):
         rng = np.random.default_rng(seed)
@@ -38,3 +43,46 @@ for dims, rank, algo, scale, grid, strict in CASES:
         print(f"dims {dims} R={rank} {algo} x*2^{scale} grid {grid} seed {seed}: reference seq vs grid trace diff "
               f"{np.max(np.abs(seq - par) / np.maximum(1.0, seq)):.2e}   (unscaled control: "
               f"{np.max(np.abs(seq1 - par1)):.2e});  eps[0..] {seq[:3]}")
+
+# What the device changes is summation order: the Gram G_n = H_n^T H_n (a reduction over
+# the mode's rows), the MTTKRP, the HALS row product.  The first update of a tensor far
+# below the initial factors' scale cancels O(1) terms of S = Hadamard(Grams) down to the
+# tensor's scale, so an ulp of S becomes a relative error of the survivors.  The oracle
+# (bit-identical to the reference on these runs) with only the Gram summed in another
+# legal order (16-, 32- or 128-row blocks in sequence instead of one BLAS dgemm; the
+# largest change of the three): the scaled runs
+# move by the order the device did, the unscaled controls by ~1e-15.
+sys.path.insert(0, ROOT)
+from oracle import nncp_oracle as O  # noqa: E402
+
+stock = O.gram
+
+
+def gram_blocked(blk):
+    def gram(h):
+        g = np.zeros((h.shape[1], h.shape[1]))
+        for i in range(0, h.shape[0], blk):
+            g = g + h[i:i + blk].T @ h[i:i + blk]
+        return 0.5 * (g + g.T)
+    return gram
+
+
+for dims, rank, algo, scale, grid, strict in CASES:
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        hs = [rng.random((d, rank)) for d in dims]
+        x = O.khatri_rao(hs) @ np.ones(rank)
+        x = (x + 0.05 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))) * 2.0 ** scale
+        out = []
+        for xx in (x, x * 2.0 ** -scale):
+            O.gram = stock
+            a = np.array(O.run_sequential(xx, dims, rank, algo, 4, 0.0, seed, strict_split=strict)[0])
+            worst = 0.0
+            for blk in (16, 32, 128):
+                O.gram = gram_blocked(blk)
+                b = np.array(O.run_sequential(xx, dims, rank, algo, 4, 0.0, seed, strict_split=strict)[0])
+                worst = max(worst, float(np.max(np.abs(a - b) / np.maximum(1.0, a))))
+            out.append(worst)
+        O.gram = stock
+        print(f"dims {dims} R={rank} {algo} x*2^{scale} seed {seed}: oracle, Gram as one dgemm vs row blocks: "
+              f"trace diff {out[0]:.2e}   (unscaled control: {out[1]:.2e})")

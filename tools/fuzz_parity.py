@@ -90,7 +90,9 @@ for case in range(cases):
         # traces compared relative to max(1, eps): a tensor scaled by 2^-60 starts at eps ~ 1e15
         dt = float(np.max(np.abs(np.array(rep.errors) - np.array(errors)) / np.maximum(1.0, np.abs(errors))))
         df = max(float(np.max(np.abs(a - b))) for a, b in zip(rep.model.factors, factors))
-        bad = dt > tol or df > 1e-6
+        keep = np.abs(lam) > 0
+        dl = float(np.max(np.abs(rep.model.lam[keep] - lam[keep]) / np.abs(lam[keep]))) if keep.any() else 0.0
+        bad = dt > tol or df > 1e-6 or dl > 1e-6
         grid_msg = ""
         if order >= 2 and rng.random() < 0.5:
             grid = tuple(int(rng.integers(1, min(d, 3) + 1)) for d in dims)
@@ -108,7 +110,7 @@ for case in range(cases):
         if bad:
             fails += 1
             print(f"  device {np.array(rep.errors)}\n  oracle {np.array(errors)}", flush=True)
-        print(f"{tag}: trace {dt:.1e} factors {df:.1e}{grid_msg}{'  <-- FAIL' if bad else ''}", flush=True)
+        print(f"{tag}: trace {dt:.1e} factors {df:.1e} lambda {dl:.1e}{grid_msg}{'  <-- FAIL' if bad else ''}", flush=True)
     except Exception:  # noqa: BLE001
         fails += 1
         print(f"{tag}: EXCEPTION\n{traceback.format_exc()}", flush=True)
