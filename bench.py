@@ -84,6 +84,8 @@ class ClockSampler:
         self.first = 0
 
     def start(self):
+        if os.environ.get("NNCP_BENCH_NO_SMI"):   # diagnostics only: the sampler's own cost
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
                                           "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,

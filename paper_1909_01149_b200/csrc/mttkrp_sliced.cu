@@ -623,13 +623,18 @@ template <int L, int NF, int H>
 int launch_bseg(const BSpec& b0, int* bexp, int8_t* bs, cudaStream_t st) {
   BSpec b = b0;
   const int64_t outer = b.K / b.dim[0], nseg = b.dim[0] / BK;
-  // >= ~4 blocks per SM (512^3: 4 segments x 512 outer indices -> 3 per block, 684 blocks)
-  b.segg = int(std::max<int64_t>(1, std::min<int64_t>(SEG_G, nseg * outer / (4 * int64_t(num_sms())))));
+  // exponent pass: >= ~4 blocks per SM (512^3: 4 segments x 512 outer indices -> 3 per
+  // block, 684 blocks); digit pass: ~8 blocks per SM but at least 3 outer indices per
+  // block (measured, tools/ncu launch lists: 1024^3 66 -> 60 us, 512^3 unchanged)
+  const int64_t work = nseg * outer, sms = num_sms();
+  b.segg = int(std::max<int64_t>(1, std::min<int64_t>(SEG_G, work / (4 * sms))));
   const dim3 grid{unsigned(nseg), unsigned((outer + b.segg - 1) / b.segg), 1u};
   bseg_exp_kernel<NF, H><<<grid, 256, 0, st>>>(b, bexp);
   NNCP_LAUNCH_CHECK();
+  b.segg = int(std::max<int64_t>(std::min<int64_t>(3, outer), std::min<int64_t>(SEG_G, work / (8 * sms))));
+  const dim3 grid_d{unsigned(nseg), unsigned((outer + b.segg - 1) / b.segg), 1u};
   if (int rc = set_max_smem_once<bseg_digits_kernel<L, NF, H>>(int(L * kMaxRank * SEG_PITCH))) return rc;
-  bseg_digits_kernel<L, NF, H><<<grid, 256, size_t(L) * b.RP * SEG_PITCH, st>>>(b, bexp, bs);
+  bseg_digits_kernel<L, NF, H><<<grid_d, 256, size_t(L) * b.RP * SEG_PITCH, st>>>(b, bexp, bs);
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

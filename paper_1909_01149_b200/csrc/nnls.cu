@@ -634,15 +634,26 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int64_t r0 = int64_t(blockIdx.x) * kGramRows;
   const int nr = int(rows - r0 < kGramRows ? rows - r0 : int64_t(kGramRows));
-  for (int e = threadIdx.x; e < nr * R; e += blockDim.x) {
-    const int il = e / R, r = e - (e / R) * R;
-    const int64_t gi = (r0 + il) * R + r;
-    double v = hhat[gi];
-    if (nsq) {
-      v = v / scale[r];
-      owned[gi] = v;
+  // every load of the tile issued before the first use (a load-use loop serialised
+  // PER global-memory latencies; this kernel is latency-bound at these sizes)
+  constexpr int PER = (kGramRows * RP + 255) / 256;
+  double v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = int(threadIdx.x) + 256 * k, il = e / RP, r = e % RP;
+    v[k] = (il < nr && r < R) ? hhat[(r0 + il) * R + r] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = int(threadIdx.x) + 256 * k, il = e / RP, r = e % RP;
+    if (il < nr && r < R) {
+      double x = v[k];
+      if (nsq) {
+        x = x / scale[r];
+        owned[(r0 + il) * R + r] = x;
+      }
+      tile[il * RP + r] = x;
     }
-    tile[il * RP + r] = v;
   }
   __syncthreads();
   if (gram == nullptr) return;  // row scaling only

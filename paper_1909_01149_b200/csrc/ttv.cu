@@ -8,7 +8,11 @@
 // are R doubles apart, so reading them per element would cost 4x the sectors of
 // T itself), T is streamed with 16-byte loads along the contiguous leading mode,
 // and every reduction is fixed-order: run-to-run bitwise deterministic.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace nncp {
 
@@ -37,9 +41,13 @@ __device__ __forceinline__ double coeff_value(const CoeffSpec& s, int64_t j, int
 
 constexpr int kTtvChunk = 4096;  // coefficient entries staged per pass (32 KB)
 
-// trailing: CTA = (tile of 128 leading rows, rank r).  Lane pairs of rows are read
-// as double2 (when the leading extent is even); the 8 warps split the trailing
-// index, 4 loads in flight per lane; partial sums combined in warp order.
+// trailing: CTA = (tile of 128 leading rows, rank r, part z of the trailing range).
+// Lane pairs of rows are read as double2 (when the leading extent is even); the 8
+// warps split the CTA's trailing indices, 4 loads in flight per lane; partial sums
+// combined in warp order.  When the leading extent is short (few row tiles) the
+// trailing range is split over the gridDim.z CTAs of a thread-block cluster, whose
+// partials CTA 0 of the cluster adds in cluster-rank order through distributed
+// shared memory: more loads in flight without a workspace, still fixed-order.
 __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restrict__ t, int64_t L, int64_t J,
                                                            const CoeffSpec cs, int R, double* __restrict__ out,
                                                            bool vec) {
@@ -49,9 +57,11 @@ __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restr
   const int r = blockIdx.y;
   const int64_t l0 = int64_t(blockIdx.x) * 128 + 2 * lane;  // this lane: rows l0, l0+1 (+64, +65)
   const double* tr = t + L * J * r;
+  const int nz = int(gridDim.z), z = int(blockIdx.z);
+  const int64_t jper = (J + nz - 1) / nz, ja = min(J, jper * z), jb = min(J, ja + jper);
   double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-  for (int64_t jc = 0; jc < J; jc += kTtvChunk) {
-    const int nj = int(J - jc < kTtvChunk ? J - jc : int64_t(kTtvChunk));
+  for (int64_t jc = ja; jc < jb; jc += kTtvChunk) {
+    const int nj = int(jb - jc < kTtvChunk ? jb - jc : int64_t(kTtvChunk));
     __syncthreads();
     for (int q = threadIdx.x; q < nj; q += blockDim.x) coef[q] = coeff_value(cs, jc + q, r, R);
     __syncthreads();
@@ -114,32 +124,54 @@ __global__ void __launch_bounds__(256) ttv_trailing_kernel(const double* __restr
       s.x += part[w][threadIdx.x].x;
       s.y += part[w][threadIdx.x].y;
     }
+    part[0][threadIdx.x] = s;
+  }
+  if (nz > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();                                   // every CTA's part[0] is complete
+    if (z == 0 && threadIdx.x < 64) {
+      double2 s = part[0][threadIdx.x];
+      for (int q = 1; q < nz; ++q) {
+        const double2 o = cl.map_shared_rank(&part[0][0], q)[threadIdx.x];
+        s.x += o.x;
+        s.y += o.y;
+      }
+      part[0][threadIdx.x] = s;
+    }
+    cl.sync();                                   // the others' shared memory stays alive until read
+    if (z != 0) return;
+  }
+  if (threadIdx.x < 64) {
+    const double2 s = part[0][threadIdx.x];
     const int64_t l = int64_t(blockIdx.x) * 128 + 2 * (threadIdx.x & 31) + 64 * (threadIdx.x >> 5);
     if (l < L) out[l + L * r] = s.x;
     if (l + 1 < L) out[l + 1 + L * r] = s.y;
   }
 }
 
-// leading: CTA = (rank r, 64 consecutive trailing indices j); H[:, r] staged in
-// shared memory per pass of kTtvChunk leading rows; each warp owns 8 j columns.
+// leading: CTA = (rank r, 8 Q consecutive trailing indices j); H[:, r] staged in
+// shared memory per pass of kTtvChunk leading rows; each warp owns Q j columns
+// (Q < 8 when 8 per warp would leave the grid short of ~4 CTAs per SM: the columns
+// of a warp are walked one after another, so fewer per warp is a shorter chain).
+template <int Q>
 __global__ void __launch_bounds__(256) ttv_leading_kernel(const double* __restrict__ t, int64_t L, int64_t J,
                                                           const double* __restrict__ h, int R,
                                                           double* __restrict__ out, bool vec) {
   __shared__ double hc[kTtvChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.y;
-  const int64_t j0 = int64_t(blockIdx.x) * 64 + warp * 8;
+  const int64_t j0 = int64_t(blockIdx.x) * (8 * Q) + warp * Q;
   const double* tr = t + L * J * r;
-  double acc[8];
+  double acc[Q];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
   for (int64_t lc = 0; lc < L; lc += kTtvChunk) {
     const int nl = int(L - lc < kTtvChunk ? L - lc : int64_t(kTtvChunk));
     __syncthreads();
     for (int q = threadIdx.x; q < nl; q += blockDim.x) hc[q] = __ldg(h + (lc + q) * R + r);
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int64_t j = j0 + q;
       if (j >= J) break;
       const double* col = tr + L * j + lc;
@@ -169,7 +201,7 @@ __global__ void __launch_bounds__(256) ttv_leading_kernel(const double* __restri
     }
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < Q; ++q) {
     const double s = warp_sum(acc[q]);
     const int64_t j = j0 + q;
     if (lane == 0 && j < J) out[j + J * r] = s;
@@ -204,12 +236,36 @@ int multi_ttv(const double* temp, int nret, const int64_t* ret_dims, int rank, i
       prod *= coeff_rows[f];
     }
     if (prod != J) return fail(NNCP_ERR_VALUE, "coeff rows do not match the trailing dimension");
-    dim3 grid(unsigned((L + 127) / 128), unsigned(rank));
-    ttv_trailing_kernel<<<grid, 256, 0, st>>>(temp, L, J, cs, rank, out, vec);
+    // split the trailing range over a cluster of up to 8 CTAs while the grid is short
+    // of ~4 CTAs per SM and every part keeps >= 64 trailing indices (8 per warp)
+    const int64_t tiles = (L + 127) / 128 * rank, target = 4 * int64_t(num_sms());
+    int nz = 1;
+    while (nz < 8 && tiles * nz < target && J / (2 * nz) >= 64) nz *= 2;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(unsigned((L + 127) / 128), unsigned(rank), unsigned(nz));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = unsigned(nz);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, ttv_trailing_kernel, temp, L, J, cs, rank, out, vec) != cudaSuccess)
+      return fail(NNCP_ERR_CUDA, "ttv_trailing_kernel launch failed");
   } else if (side == NNCP_TTV_LEADING) {
     if (ncoeff != 1 || coeff_rows[0] != L) return fail(NNCP_ERR_VALUE, "coeff rows do not match the leading dimension");
-    dim3 grid(unsigned((J + 63) / 64), unsigned(rank));
-    ttv_leading_kernel<<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec);
+    const int64_t target = 4 * int64_t(num_sms());
+    int q = 8;
+    while (q > 1 && (J + 8 * q - 1) / (8 * q) * rank < target) q /= 2;
+    const dim3 grid(unsigned((J + 8 * q - 1) / (8 * q)), unsigned(rank));
+    switch (q) {
+      case 8: ttv_leading_kernel<8><<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec); break;
+      case 4: ttv_leading_kernel<4><<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec); break;
+      case 2: ttv_leading_kernel<2><<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec); break;
+      default: ttv_leading_kernel<1><<<grid, 256, 0, st>>>(temp, L, J, coeff[0], rank, out, vec); break;
+    }
   } else {
     return fail(NNCP_ERR_VALUE, "side must be trailing or leading");
   }
