@@ -526,7 +526,8 @@ def main():
                         "through the engine): tensor H2D once per call of "
                         f"{args.steps} iterations + init + D2H of the model, divided by the steps"},
         "gpu_launches": res["launches"],
-        "collectives": ({"backend": "nccl", "env": res["nccl_env"], "merged_norm_gram": res["merged_norm_gram"]}
+        "collectives": ({"backend": os.environ.get("NNCP_DIST_BACKEND", "nccl"), "env": res["nccl_env"],
+                         "merged_norm_gram": res["merged_norm_gram"]}
                         if res["world"] > 1 else None),
         "clocks": res["clocks"],
         "final_error": res["errors"][-1],
