@@ -63,6 +63,35 @@ def test_partials_and_ttv_vs_golden(P, golden):
             assert rel_fro(_np(lead.data), g[f"c{k}_ttv_lead"]) <= MTTKRP_TOL, k
 
 
+@pytest.mark.parametrize("lead,trail,rank", [
+    (100, (64, 64), 3),      # one row tile, 3 ranks: trailing range split over an 8-CTA cluster
+    (512, (512,), 16),       # c2's shape: 4 tiles x 16 ranks, cluster of 8; leading 1 column per warp
+    (257, (33, 31), 5),      # ragged everything, odd leading extent (scalar loads)
+    (2048, (8,), 32),        # short trailing range: no split
+])
+def test_multi_ttv_grid_variants_vs_oracle(P, lead, trail, rank):
+    """Both multi-TTV kernels at shapes that pick each launch variant (trailing split over a
+    thread-block cluster with a DSMEM fixed-order sum; leading with 8/4/2/1 columns per
+    warp), against the oracle; and bitwise run-to-run."""
+    import torch
+
+    rng = np.random.default_rng(lead + rank)
+    J = int(np.prod(trail))
+    t = rng.random(lead * J * rank)
+    coeffs = [rng.random((d, rank)) for d in trail]
+    c0 = rng.random((lead, rank))
+    temp = P.TempTensor((lead,) + tuple(trail), rank, torch.as_tensor(t, device="cuda"))
+    krp = O.khatri_rao(coeffs)
+    a = _np(P.multi_ttv(temp, coeffs, "trailing").data)
+    b = _np(P.multi_ttv(temp, coeffs, "trailing").data)
+    assert np.array_equal(a, b)
+    assert rel_fro(a, O.ttv_trailing(t, lead, rank, krp)) <= MTTKRP_TOL
+    a = _np(P.multi_ttv(temp, c0, "leading").data)
+    b = _np(P.multi_ttv(temp, c0, "leading").data)
+    assert np.array_equal(a, b)
+    assert rel_fro(a, O.ttv_leading(t, lead, rank, c0)) <= MTTKRP_TOL
+
+
 def test_dimtree_all_modes_vs_golden(P, golden):
     g = golden("mttkrp.npz")
     for k in range(int(g["ncases"])):
