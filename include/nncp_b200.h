@@ -108,6 +108,17 @@ int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dim
                                const double* const* factors, int rank, int levels, double* out, void* ws,
                                size_t ws_bytes, void* stream);
 
+/* nncp_partial_mttkrp_sliced without the final split-K group reduction: when the
+ * contraction was split into groups (*groups_out > 1) the group partials stay in the
+ * workspace at *parts_out (column-major (rows, R) each, *gstride_out doubles apart) for a
+ * consumer that sums them itself (nncp_update_grouped: the last mode's MTTKRP of a
+ * 3-way tree is the right partial itself); otherwise out is written and
+ * *parts_out = out, *groups_out = 1.  One launch fewer per sweep. */
+int nncp_partial_mttkrp_sliced_deferred(const void* sliced, int order, const int64_t* dims, int split, int side,
+                                        const double* const* factors, int rank, int levels, double* out, void* ws,
+                                        size_t ws_bytes, const double** parts_out, int* groups_out,
+                                        int64_t* gstride_out, void* stream);
+
 /* The left sliced partial plus the dimension tree's first trailing multi-TTV in one
  * pass (dimtree.py:241-250 mode 1: out_trailing = multi_ttv(T_L, H_2, trailing)),
  * accumulated in the GEMM epilogue instead of re-reading T_L.  Supported for split 2,
@@ -169,6 +180,14 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
                    int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
                    void* stream);
+/* nncp_update_ex with M given as m_groups column-major partials (leading dimension
+ * m_ld >= rows, m_gstride >= m_ld * rank doubles apart) summed in group order while the
+ * rows are loaded -- the output of nncp_partial_mttkrp_sliced_deferred.  MU, HALS, BPP.
+ * The partials must not overlap the workspace's tickets and per-CTA partials. */
+int nncp_update_grouped(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_parts,
+                        int64_t m_ld, int m_groups, int64_t m_gstride, const double* owned, const double* lam,
+                        int64_t rows, double* hhat, double* nsq, double* beta, int* status, double mu_eps,
+                        void* bpp_sets, void* ws, size_t ws_bytes, void* stream);
 /* nncp_update_ex followed, in the same launch, by the normalisation of
  * nncp_normalize_gram (driver.py:411-422) for a single context: the kernel's last CTA
  * turns the column sums into w = sqrt(nsq), writes owned = hhat / (w > 0 ? w : 1),

@@ -53,6 +53,9 @@ SIGNATURES = [
     ("nncp_partial_mttkrp_sliced", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, vp,
       vp, ctypes.c_size_t, vp]),
+    ("nncp_partial_mttkrp_sliced_deferred", ctypes.c_int,
+     [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, vp,
+      vp, ctypes.c_size_t, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64), vp]),
     ("nncp_sliced_trailing_supported", ctypes.c_int,
      [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("nncp_partial_mttkrp_sliced_trailing", ctypes.c_int,
@@ -71,6 +74,9 @@ SIGNATURES = [
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
       ctypes.c_double, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp,
       ctypes.c_size_t, vp]),
+    ("nncp_update_grouped", ctypes.c_int,
+     [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+      vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_double, vp, vp, ctypes.c_size_t, vp]),
     ("nncp_update_ex", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
       ctypes.c_double, vp, ctypes.c_int64, vp, ctypes.c_size_t, vp]),

@@ -59,7 +59,8 @@ size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int 
 bool sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels);
 int slice_tensor(const double*, int, const int64_t*, int, int, void*, size_t, cudaStream_t);
 int sliced_partial_mttkrp(const void*, int, const int64_t*, int, int, const double* const*, int, int, double*, double*,
-                          void*, size_t, cudaStream_t);
+                          void*, size_t, cudaStream_t, const double** parts_out = nullptr, int* groups_out = nullptr,
+                          int64_t* gstride_out = nullptr);
 
 // caller buffers for the sliced path are used from the next 1 KB boundary on
 static inline void* align1k(const void* p, size_t bytes, size_t* avail) {
@@ -184,6 +185,23 @@ int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dim
                                S(stream));
 }
 
+int nncp_partial_mttkrp_sliced_deferred(const void* sliced, int order, const int64_t* dims, int split, int side,
+                                        const double* const* factors, int rank, int levels, double* out, void* ws,
+                                        size_t ws_bytes, const double** parts_out, int* groups_out,
+                                        int64_t* gstride_out, void* stream) {
+  int rc = check_common(order, dims, rank);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (side != NNCP_SIDE_LEFT && side != NNCP_SIDE_RIGHT)
+    return fail(NNCP_ERR_VALUE, "side must be 'left' or 'right'");
+  if (!sliced || !parts_out || !groups_out || !gstride_out) return fail(NNCP_ERR_VALUE, "null argument");
+  size_t dummy = 0, avail = 0;
+  const void* base = align1k(sliced, 1024, &dummy);
+  void* w = (ws && ws_bytes > 256) ? align1k(static_cast<char*>(ws) + 256, ws_bytes - 256, &avail) : nullptr;
+  return sliced_partial_mttkrp(base, order, dims, split, side, factors, rank, levels, out, nullptr, w, avail,
+                               S(stream), parts_out, groups_out, gstride_out);
+}
+
 int nncp_sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels) {
   if (order < 2 || order > kMaxOrder || rank < 1 || rank > kMaxRank || split < 1 || split >= order) return 0;
   for (int n = 0; n < order; ++n)
@@ -232,8 +250,16 @@ int nncp_status_reset_n(int* status, int count, void* stream) {
 static int update_dispatch(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,
                            const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq,
                            double* beta, int* status, double mu_eps, void* bpp_sets, int64_t m_ld, const TailArgs* tail,
-                           void* ws, size_t ws_bytes, void* stream) {
+                           void* ws, size_t ws_bytes, void* stream, int m_groups = 1, int64_t m_gstride = 0) {
   if (m_ld < 0 || (m_ld > 0 && m_ld < rows)) return fail(NNCP_ERR_VALUE, "m_ld must be 0 (row-major) or >= rows");
+  if (m_groups < 1 || (m_groups > 1 && (m_ld == 0 || m_gstride < m_ld * rank)))
+    return fail(NNCP_ERR_VALUE, "group partials need m_ld > 0 and m_gstride >= m_ld * rank");
+  if (m_groups > 1 && algo != NNCP_ALGO_MU && algo != NNCP_ALGO_HALS && algo != NNCP_ALGO_BPP)
+    return fail(NNCP_ERR_UNSUPPORTED, "group partials: MU, HALS or BPP");
+  TailArgs targs = tail ? *tail : TailArgs{};
+  targs.mgroups = m_groups;
+  targs.mgstride = m_gstride;
+  tail = &targs;
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64] on the device path");
   if (order < 0 || order > kMaxOrder) return fail(NNCP_ERR_VALUE, "bad order");
   if (order > 0 && (mode < 0 || mode >= order)) return fail(NNCP_ERR_VALUE, "exclude index out of range");
@@ -257,6 +283,14 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
                    void* stream) {
   return update_dispatch(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, mu_eps,
                          bpp_sets, m_ld, nullptr, ws, ws_bytes, stream);
+}
+
+int nncp_update_grouped(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_parts,
+                        int64_t m_ld, int m_groups, int64_t m_gstride, const double* owned, const double* lam,
+                        int64_t rows, double* hhat, double* nsq, double* beta, int* status, double mu_eps,
+                        void* bpp_sets, void* ws, size_t ws_bytes, void* stream) {
+  return update_dispatch(algo, grams, order, mode, rank, mttkrp_parts, owned, lam, rows, hhat, nsq, beta, status,
+                         mu_eps, bpp_sets, m_ld, nullptr, ws, ws_bytes, stream, m_groups, m_gstride);
 }
 
 int nncp_update_normalize(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_rows,

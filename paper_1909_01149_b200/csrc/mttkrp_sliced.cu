@@ -1307,7 +1307,8 @@ int slice_tensor(const double* x, int order, const int64_t* dims, int split, int
 
 int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, int split, int side,
                           const double* const* factors, int rank, int levels, double* out, double* out_trailing,
-                          void* ws, size_t ws_bytes, cudaStream_t st) {
+                          void* ws, size_t ws_bytes, cudaStream_t st, const double** parts_out, int* groups_out,
+                          int64_t* gstride_out) {
   using namespace sliced;
   if (int rc = check_levels(levels)) return rc;
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "sliced MTTKRP: rank outside [1, 64]");
@@ -1417,7 +1418,12 @@ int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, 
   int rc = levels == 6 ? dispatch_gemm<6>(side, p.RP, ma, mb, mo, ga, st)
                        : dispatch_gemm<7>(side, p.RP, ma, mb, mo, ga, st);
   if (rc) return rc;
-  if (p.groups > 1) {
+  if (parts_out != nullptr) {
+    // deferred: the consumer (nncp_update_grouped) sums the group partials itself
+    *parts_out = ga.out;
+    *groups_out = p.groups;
+    *gstride_out = p.groups > 1 ? ga.group_stride : 0;
+  } else if (p.groups > 1) {
     const int64_t n = p.rows * rank;
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
     group_reduce_kernel<<<blocks, 256, 0, st>>>(ga.out, p.groups, n, n, out);

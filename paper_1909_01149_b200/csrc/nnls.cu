@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
       const int r = lane + 32 * q;
       h[q] = (r < R) ? (lam ? orow[r] * lam[r] : orow[r]) : 0.0;  // driver.py:403 current = owned * lam
       // M row-major, or (mld > 0) the dimension tree's column-major temporary itself
-      m[q] = (r < R) ? (mld ? mrows[i + mld * r] : mr[r]) : 0.0;
+      m[q] = (r < R) ? load_m(mrows, mld, i, r, R, tail) : 0.0;
     }
     if (ALGO == NNCP_ALGO_MU) {
       // updaters.py:93-94: current * M / (current @ S + eps)
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 #pragma unroll
     for (int q = 0; q < NH; ++q) {
       const int r = lane + 32 * q;
-      fs[q] = (r < R) ? (mld ? mrows[i + mld * r] : mrows[i * R + r]) : 0.0;
+      fs[q] = (r < R) ? load_m(mrows, mld, i, r, R, tail) : 0.0;
       xs[q] = 0.0;
       ys[q] = -fs[q];
       if (r < R) fbuf[r] = fs[q];
@@ -875,6 +875,17 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
   WsLayout w = ws_layout(ws, ws_bytes);
   const int rp = pad8(rank);
   (void)rp;
+  if (tl.mgroups > 1) {
+    // group partials may live in the same workspace (the sliced MTTKRP's): they must not
+    // meet the tickets and per-CTA partials this launch writes
+    const char* m0 = reinterpret_cast<const char*>(mrows);
+    const char* m1 = m0 + sizeof(double) * size_t(tl.mgroups) * size_t(tl.mgstride);
+    const char* w0 = static_cast<const char*>(ws);
+    const char* w1 = reinterpret_cast<const char*>(w.part + size_t(std::max<int64_t>(row_blocks(rows), num_sms())) *
+                                                   (rank + 1));
+    if (m0 < w1 && w0 < m1) return fail(NNCP_ERR_VALUE, "group partials overlap the update's workspace");
+    if (mld < rows || tl.mgstride < mld * rank) return fail(NNCP_ERR_VALUE, "bad group partial layout");
+  }
   if (algo == NNCP_ALGO_MU || algo == NNCP_ALGO_HALS) {
     const int blocks = row_blocks(rows);
     if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (update)");

@@ -206,7 +206,23 @@ struct TailArgs {
   double* gram;
   double* scratch;        // >= max(64 R, R^2 + R) doubles of shared memory
   PublishArgs pub;        // pub.gamma == nullptr: no gamma / hand-off
+  // M as split-K group partials left by the sliced partial MTTKRP (column-major,
+  // m_ld apart per column, mgstride apart per group): the update sums them in group
+  // order while loading its rows (group_reduce_kernel's arithmetic, one launch fewer)
+  int mgroups;            // <= 1: M itself
+  int64_t mgstride;
 };
+
+// Element (i, r) of M: row-major (mld == 0), or column-major with leading dimension
+// mld, optionally the sum over t.mgroups group partials in group order.
+__device__ __forceinline__ double load_m(const double* __restrict__ mrows, int64_t mld, int64_t i, int r, int R,
+                                         const TailArgs& t) {
+  if (!mld) return mrows[i * R + r];
+  const double* p = mrows + i + mld * r;
+  double s = p[0];
+  for (int g = 1; g < t.mgroups; ++g) s += p[g * t.mgstride];
+  return s;
+}
 
 static __device__ void fused_tail(const TailArgs& t, int R, const double* nsq_s /* shared, R */, double* scale) {
   for (int r = threadIdx.x; r < R; r += blockDim.x) {

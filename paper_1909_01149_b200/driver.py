@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dimtree import DimTreeContext, DimTreePlan, SlicedTensor, choose_balanced_split
+from .dimtree import DeferredPartial, DimTreeContext, DimTreePlan, SlicedTensor, choose_balanced_split
 from .grid import (CommCounters, DistCollectives, Grid, IdentityCollectives, RankLayout, ThreadCollectives,
                    ThreadGrid, block_partition)
 from .tensor_ops import DenseTensor, FactorSet, Workspace, as_device
@@ -600,10 +600,19 @@ class _Engine:
         for n in range(N):
             mb = self.mbar[: self.dims[n]]
             m_ld = 0
+            rows_n = self.n_owned[n]
+            fused_tail = in_place and R <= 32 and 1 <= rows_n and rows_n * R * R <= FUSED_TAIL_MAX
+            grouped = None
             if in_place:
-                temp = (self.ctx.mttkrp(self.x, self.shared, n, rows=False) if cfg.use_dimtree
+                # a sliced root partial may hand its split-K groups to the update (one
+                # launch fewer: nncp_update_grouped sums them while loading the rows)
+                defer = cfg.use_dimtree and not fused_tail and cfg.algorithm in ("mu", "hals", "bpp")
+                temp = (self.ctx.mttkrp(self.x, self.shared, n, rows=False, defer_groups=defer) if cfg.use_dimtree
                         else self.ctx.mttkrp_direct(self.x, self.shared, n, rows=False))
-                mb, m_ld = temp.data, self.dims[n]
+                if isinstance(temp, DeferredPartial):
+                    grouped, m_ld = temp, self.dims[n]
+                else:
+                    mb, m_ld = temp.data, self.dims[n]
             elif cfg.use_dimtree:
                 self.ctx.mttkrp(self.x, self.shared, n, out=mb)
             else:
@@ -612,8 +621,7 @@ class _Engine:
             m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
             self._cmark("ReduceScatter")
             last = n == N - 1
-            rows_n = self.n_owned[n]
-            if in_place and R <= 32 and 1 <= rows_n and rows_n * R * R <= FUSED_TAIL_MAX:
+            if fused_tail:
                 # small single-context block: the update kernel's last CTA also normalises,
                 # forms the Gram (and for the last mode gamma + the status hand-off)
                 _lib.check(lib.nncp_update_normalize(
@@ -627,7 +635,15 @@ class _Engine:
                 self.timer.mark("NNLS")
                 published = published or last
                 continue
-            if cfg.algorithm in FUSED_ALGORITHMS:
+            if grouped is not None:
+                _lib.check(lib.nncp_update_grouped(self.algo, _lib.ptr(self.grams), N, n, R, grouped.ptr, m_ld,
+                                                   grouped.groups, grouped.gstride, _lib.ptr(self.owned[n]),
+                                                   _lib.ptr(self.lam), rows_n, _lib.ptr(self.hhat),
+                                                   _lib.ptr(self.nsq), _lib.ptr(self.xvec) if last else None,
+                                                   _lib.ptr(self.status[n]), 1e-16,
+                                                   _lib.ptr(self.bpp_sets[n]) if self.bpp_sets else None,
+                                                   self.ws.ptr, self.ws.nbytes, st))
+            elif cfg.algorithm in FUSED_ALGORITHMS:
                 _lib.check(lib.nncp_update_ex(self.algo, _lib.ptr(self.grams), N, n, R, _lib.ptr(m_owned),
                                               _lib.ptr(self.owned[n]), _lib.ptr(self.lam), self.n_owned[n],
                                               _lib.ptr(self.hhat), _lib.ptr(self.nsq),

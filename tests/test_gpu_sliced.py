@@ -378,3 +378,65 @@ def test_non_finite_tensor_uses_fp64_engine(P):
         eng = _Engine(xd, dims, dims, P.RunConfig(rank=r, algorithm="hals", max_iters=1, mttkrp_kernel="sliced"),
                       IdentityCollectives())
     assert eng.sliced is None and not eng.facts.finite
+
+
+@pytest.mark.parametrize("algo", ["hals", "mu", "bpp"])
+@pytest.mark.parametrize("dims,side", [((256, 256, 128), "right"), ((300, 64, 48), "right"),
+                                       ((1024, 256, 256), "left")])
+def test_deferred_groups_feed_the_update_bitwise(P, algo, dims, side):
+    """nncp_partial_mttkrp_sliced_deferred + nncp_update_grouped (the update sums the
+    split-K group partials while loading its rows) == nncp_partial_mttkrp_sliced (group
+    reduction kernel) + nncp_update_ex on the reduced temporary, bit for bit."""
+    import torch
+
+    from paper_1909_01149_b200 import _lib
+    from paper_1909_01149_b200.dimtree import DeferredPartial
+    from paper_1909_01149_b200.tensor_ops import Workspace
+
+    r = 16
+    rng = np.random.default_rng(sum(dims))
+    x = P.DenseTensor(dims, rng.random(int(np.prod(dims)))).to_device()
+    split = 1 if side == "left" else 2
+    plan = P.DimTreePlan.create(dims, r) if split == 2 else P.DimTreePlan(dims=dims, rank=r, split=1)
+    assert plan.split == split
+    sl = _sliced(P, x, plan)
+    hs = [torch.as_tensor(rng.random((d, r)), device="cuda") for d in dims]
+    ws = Workspace(plan.sliced_workspace_bytes(6))
+    mode = 0 if side == "left" else 2
+    rows = dims[mode]
+    d = P.partial_mttkrp(x, hs, side, plan, workspace=ws, sliced=sl, defer=True)
+    assert isinstance(d, DeferredPartial) and d.groups > 1, "shape must split the contraction into groups"
+    lib, st = _lib.load(), _lib.stream_handle()
+    grams = torch.stack([h.T @ h for h in hs]).contiguous()
+    cur = torch.as_tensor(rng.random((rows, r)), device="cuda")
+    status = torch.zeros((2, _lib.STATUS_WORDS), dtype=torch.int32, device="cuda")
+    uws = Workspace(1 << 22)
+    outs = []
+    for k in range(2):
+        hhat = torch.empty((rows, r), dtype=torch.float64, device="cuda")
+        nsq = torch.empty(r, dtype=torch.float64, device="cuda")
+        beta = torch.zeros(1, dtype=torch.float64, device="cuda")
+        sets = torch.zeros(rows, dtype=torch.int64, device="cuda") if algo == "bpp" else None
+        if k == 0:
+            _lib.check(lib.nncp_update_grouped(_lib.ALGO_CODES[algo], _lib.ptr(grams), 3, mode, r, d.ptr, rows,
+                                               d.groups, d.gstride, _lib.ptr(cur), None, rows, _lib.ptr(hhat),
+                                               _lib.ptr(nsq), _lib.ptr(beta), _lib.ptr(status[k]), 1e-16,
+                                               _lib.ptr(sets) if sets is not None else None, uws.ptr, uws.nbytes,
+                                               st))
+        else:
+            t = P.partial_mttkrp(x, hs, side, plan, workspace=ws, sliced=sl)
+            _lib.check(lib.nncp_update_ex(_lib.ALGO_CODES[algo], _lib.ptr(grams), 3, mode, r, _lib.ptr(t.data),
+                                          _lib.ptr(cur), None, rows, _lib.ptr(hhat), _lib.ptr(nsq), _lib.ptr(beta),
+                                          _lib.ptr(status[k]), 1e-16,
+                                          _lib.ptr(sets) if sets is not None else None, rows, uws.ptr, uws.nbytes,
+                                          st))
+        torch.cuda.synchronize()
+        outs.append((hhat.cpu().numpy(), nsq.cpu().numpy(), beta.cpu().numpy()))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    # the group partials overlapping the update's own scratch are refused
+    with pytest.raises(ValueError):
+        _lib.check(lib.nncp_update_grouped(_lib.ALGO_CODES[algo], _lib.ptr(grams), 3, mode, r,
+                                           _lib.vp(uws.ptr.value + 4096), rows, 2, rows * r, _lib.ptr(cur), None, rows,
+                                           _lib.ptr(hhat), _lib.ptr(nsq), None, _lib.ptr(status[0]), 1e-16, None,
+                                           uws.ptr, uws.nbytes, st))
