@@ -119,7 +119,7 @@ def test_c07_error_identity_matches_reconstruction(P):
 
 
 def test_c03_sequential_parallel_equivalence(P):
-    """test_acceptance.py:88-107: 6 algorithms x 4 grids within 1e-10 (NES 5e-8, see test_gpu_stateful)."""
+    """test_acceptance.py:88-107: 6 algorithms x 4 grids within 1e-10."""
     x, _ = P.generate_synthetic(P.SyntheticSpec((8, 8, 8), 2, seed=7))
     for algo in ("ucp", "mu", "hals", "bpp", "admm", "nes"):
         with warnings.catch_warnings():
@@ -130,7 +130,7 @@ def test_c03_sequential_parallel_equivalence(P):
                                                      grid=grid))
                 assert len(par.errors) == len(seq.errors)
                 diff = np.abs(np.array(par.errors) - np.array(seq.errors)).max()
-                assert diff <= (5e-8 if algo == "nes" else 1e-10), (algo, grid, diff)
+                assert diff <= 1e-10, (algo, grid, diff)
 
 
 def test_c08_communication_accounting(P):

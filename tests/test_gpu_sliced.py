@@ -156,15 +156,15 @@ def test_sliced_runs_vs_golden(P, golden):
         ref = g[f"{name}_errors"]
         got = np.array(rep.errors)
         k = min(11, len(ref))
-        tol = TRACE_TOL if algo != "nes" else 5e-8   # NES: documented discontinuities (test_gpu_stateful.py)
-        assert np.max(np.abs(got[:k] - ref[:k])) <= tol, (name, np.max(np.abs(got[:k] - ref[:k])))
-        if algo != "nes":
-            for n in range(len(dims)):
-                assert np.max(np.abs(rep.model.factors[n] - g[f"{name}_f{n}"])) <= FACTOR_TOL, (name, n)
+        assert np.max(np.abs(got[:k] - ref[:k])) <= TRACE_TOL, (name, np.max(np.abs(got[:k] - ref[:k])))
+        for n in range(len(dims)):
+            assert np.max(np.abs(rep.model.factors[n] - g[f"{name}_f{n}"])) <= FACTOR_TOL, (name, n)
 
 
 @pytest.mark.parametrize("dims,r,algo,iters", [((128, 128, 128), 16, "hals", 8), ((32, 32, 32, 32), 32, "bpp", 4),
-                                               ((256, 128, 16), 20, "hals", 6), ((96, 80, 64), 64, "mu", 5)])
+                                               ((256, 128, 16), 20, "hals", 6), ((96, 80, 64), 64, "mu", 5),
+                                               ((128, 96, 80), 16, "nes", 10), ((64, 48, 40, 8), 8, "nes", 8),
+                                               ((128, 96, 80), 16, "admm", 6)])
 def test_sliced_runs_vs_oracle(P, dims, r, algo, iters):
     rng = np.random.default_rng(sum(dims) * r)
     hs = [rng.random((d, r)) for d in dims]
