@@ -404,6 +404,23 @@ def first_failure(vec, nranks: int, order: int):
 _FAULT_ENV = "NNCP_TEST_INJECT_FAULT"
 
 
+def _state_arena(parts, dev):
+    """One zeroed device allocation holding every (shape, dtype) of ``parts`` at 256-byte
+    aligned offsets; returns (the byte buffer, typed views in order)."""
+    offs, nbytes = [], 0
+    for shape, dtype in parts:
+        offs.append(nbytes)
+        size = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        nbytes += (size + 255) // 256 * 256
+    buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=dev)
+    views = []
+    for (shape, dtype), off in zip(parts, offs):
+        esize = torch.empty((), dtype=dtype).element_size()
+        count = int(np.prod(shape))
+        views.append(buf[off:off + count * esize].view(dtype).view(shape))
+    return buf, views
+
+
 class _Engine:
     """One execution context (one GPU, or one simulated worker) of the SPMD program."""
 
@@ -459,8 +476,6 @@ class _Engine:
         # partials -> "MTTKRP", TTVs -> "MultiTTV" (the reference's recorder, dimtree.py:209-233)
         self.ctx.marker = self.timer.mark if timing else None
         R, N = self.R, self.N
-        self.grams = torch.zeros((N, R, R), **f64)
-        self.lam = torch.ones(R, **f64)
         self.nsq = torch.zeros(R, **f64)
         # grid runs over NCCL: norm + Gram All-Reduces merged into one (DistCollectives)
         self.merge_norm_gram = bool(getattr(coll, "merge_norm_gram", False))
@@ -481,20 +496,28 @@ class _Engine:
         self.masks = torch.zeros(2 * N, dtype=torch.int32, device=dev)
         # BPP: every owned row's final passive set, the next outer iteration's start
         # (nncp_update_ex; same final solve as the reference's cold start, fewer passes)
-        self.bpp_sets = ([torch.zeros(max(self.n_owned[n], 1), dtype=torch.int64, device=dev) for n in range(N)]
-                         if cfg.algorithm == "bpp" and cfg.bpp_warm_start else None)
         fault = os.environ.get(_FAULT_ENV)
         self.fault = tuple(int(v) for v in fault.split(":")) if fault else None
         self.mbar = torch.empty((max(self.dims), R), **f64)
         self.hhat = torch.empty((max(max(self.n_owned), 1), R), **f64)
-        self.owned = [torch.empty((self.n_owned[n], R), **f64) for n in range(N)]
+        # the state one sweep hands to the next -- factors, lambda, Grams, BPP passive
+        # sets -- lives in ONE allocation, so a single copy snapshots it (run-ahead replays)
+        bpp = cfg.algorithm == "bpp" and cfg.bpp_warm_start
+        parts = [((self.n_owned[n], R), torch.float64) for n in range(N)]
         if coll.parallel:
-            self.shared = [torch.empty((self.dims[n], R), **f64) for n in range(N)]
-        else:
-            self.shared = self.owned
-        self.host_scal = torch.zeros(2, dtype=torch.float64).pin_memory()
-        self.host_xvec = torch.zeros(1 + self.nranks * N, dtype=torch.float64).pin_memory()
-        self.host_masks = torch.zeros(2 * N, dtype=torch.int32).pin_memory()
+            parts += [((self.dims[n], R), torch.float64) for n in range(N)]
+        parts += [((R,), torch.float64), ((N, R, R), torch.float64)]
+        if bpp:
+            parts += [((max(self.n_owned[n], 1),), torch.int64) for n in range(N)]
+        self.state, views = _state_arena(parts, dev)
+        self.state_backup = torch.empty_like(self.state)
+        self.owned = views[:N]
+        self.shared = views[N:2 * N] if coll.parallel else self.owned
+        k = 2 * N if coll.parallel else N
+        self.lam, self.grams = views[k], views[k + 1]
+        self.lam.fill_(1.0)
+        self.bpp_sets = views[k + 2:] if bpp else None
+        self.host_scal, self.host_xvec, self.host_masks = self._host_buffers()
         # stateful rules (updaters.py:56-68): per-mode ADMM dual / Nesterov centre
         rows_max = max(max(self.n_owned), 1)
         if cfg.algorithm in ("admm", "nes"):
@@ -505,7 +528,7 @@ class _Engine:
             else:
                 self.runner = NesterovRunner(rows_max, R, dev, self.ws)
                 self.nes_prev = [None] * N
-        self.graphs = []            # [(CUDA graph of one sweep, its timing marks)]
+        self.graphs = []            # [(CUDA graph of one sweep, its timing marks, its read-back buffers)]
         # capture stream created up front: torch's first Stream() builds its stream pool
         # (~14 ms, measured), which here overlaps an asynchronous tensor upload
         self.capture_stream = torch.cuda.Stream() if cfg.cuda_graph is not False else None
@@ -793,20 +816,28 @@ class _Engine:
                                      self.ws.ptr, self.ws.nbytes, st))
             self.coll.all_reduce(self.grams[n])
 
-    def _finish_iteration(self, it):
-        torch.cuda.current_stream().synchronize()
-        masks = self.host_masks.tolist()
+    def _finish_iteration(self, it, host=None, done=None):
+        """Warnings, the failure hand-off and eps of sweep ``it`` from its read-back buffers
+        (``host``; the eager buffers by default) once ``done`` (default: the stream) is reached."""
+        host_scal, host_xvec, host_masks = host if host is not None else (self.host_scal, self.host_xvec,
+                                                                          self.host_masks)
+        if done is not None:
+            done.synchronize()
+        else:
+            torch.cuda.current_stream().synchronize()
+        masks = host_masks.tolist()
         for n in range(self.N):
             warn_for_status(masks[2 * n], masks[2 * n + 1], self.cfg.algorithm)
-        vec = self.host_xvec.tolist()
+        vec = host_xvec.tolist()
         fail = first_failure(vec, self.nranks, self.N)
         if fail is not None:
             n, kind, row = fail
+            torch.cuda.current_stream().synchronize()     # a run-ahead replay may still be in flight
             try:
                 raise_for_code(kind, row)
             except Exception as exc:
                 raise RuntimeError(f"NNLS update failed at iteration {it}, mode {n + 1}") from exc
-        return _eps_from_terms(self.alpha, vec[0], self.host_scal[1].item())
+        return _eps_from_terms(self.alpha, vec[0], host_scal[1].item())
 
     def iterate(self, count: int = None):
         """Run up to ``count`` more outer iterations (default: the rest of max_iters)."""
@@ -817,29 +848,30 @@ class _Engine:
         use_graph = (capturable and (cfg.cuda_graph is None or bool(cfg.cuda_graph))) and self.fault is None
         done = len(errors) - 1
         stop = cfg.max_iters if count is None else min(cfg.max_iters, done + count)
-        pending = None      # (marks, row) of the previous graph replay, read while the next one runs
+        ahead = None        # the replay launched for iteration it+1 before iteration it's stop test
         for it in range(done + 1, stop + 1):
             self.report.begin_row()
             wall0 = time.perf_counter()
             if use_graph and not self.graphs and it > 1 and not self.graph_failed:
                 self._capture_graphs()
             if self.graphs:
-                g, marks = self.graphs[self.graph_replays % len(self.graphs)]
-                g.replay()
+                cur = ahead if ahead is not None else self._launch_replay()
+                # run ahead: queue sweep it+1 behind sweep it, so the GPU works while the
+                # host waits for eps_it; undone (state restored from the replay's own
+                # snapshot) if sweep it turns out to be the last
+                ahead = self._launch_replay() if it + 1 <= stop else None
+                marks, host, done_ev = cur
+                eps = self._finish_iteration(it, host, done_ev)
                 self.coll.counters.add(self.graph_comm)
-                self.graph_replays += 1
                 if cfg.use_dimtree:
                     self.ctx.partial_calls += 2
-                if pending is not None:          # the GPU is busy with this replay meanwhile
-                    self.timer.collect_marks(*pending)
-                pending = (marks, self.report.rows[-1])
+                self.timer.collect_marks(marks, self.report.rows[-1])   # sweep it+1 runs meanwhile
             else:
                 self.timer.start()
                 if cfg.algorithm == "nes":
                     self._snapshot()
                 self._sweep()
-            eps = self._finish_iteration(it)
-            if not self.graphs:
+                eps = self._finish_iteration(it)
                 self.timer.collect(self.report.rows[-1])
             errors.append(eps)
             if cfg.algorithm == "nes":
@@ -848,10 +880,21 @@ class _Engine:
             self.report.row_words[-1] = self.coll.counters.total_words() - sum(self.report.row_words[:-1])
             if eps <= cfg.tol:
                 self.report.converged = True
+                if ahead is not None:
+                    self.state.copy_(self.state_backup)     # undo the run-ahead sweep
+                    torch.cuda.current_stream().synchronize()
                 break
-        if pending is not None:
-            self.timer.collect_marks(*pending)
         self.report.tree_partial_calls = self.ctx.partial_calls if cfg.use_dimtree else 0
+
+    def _launch_replay(self):
+        """Replay the next copy of the sweep graph; (its timing marks, its read-back
+        buffers, an event marking its end)."""
+        g, marks, host = self.graphs[self.graph_replays % len(self.graphs)]
+        g.replay()
+        done = torch.cuda.Event()
+        done.record()
+        self.graph_replays += 1
+        return marks, host, done
 
     @property
     def graph(self):
@@ -869,19 +912,15 @@ class _Engine:
         self.graphs = []
 
     def _capture_graphs(self):
-        """Two copies of the sweep graph with their own timing events, replayed alternately:
-        the host reads one replay's category events while the GPU runs the next, so the
-        per-iteration gap between replays is only the eps read-back (one graph when the
-        timing events are off)."""
-        first = self._capture()
-        if first is None:
-            return
-        graphs = [first]
-        if self.timer.enabled:
-            second = self._capture()
-            if second is None:
+        """Two copies of the sweep graph, each with its own timing events and pinned
+        read-back buffers, replayed alternately: sweep i+1 is launched before the host
+        reads sweep i's error (run-ahead), so the GPU never idles on the stop test."""
+        graphs = []
+        for _ in range(2):
+            cap = self._capture()
+            if cap is None:
                 return
-            graphs.append(second)
+            graphs.append(cap)
         self.graphs = graphs
 
     def _capture(self):
@@ -896,11 +935,18 @@ class _Engine:
         # capture_begin/end directly: torch.cuda.graph's context manager also empties
         # the allocator caches (device and pinned host), which this capture does not
         # need -- every buffer of the sweep already exists after sweep 1
+        # each captured copy D2H-copies into its own pinned buffers: a run-ahead replay of
+        # the other copy must not overwrite what the host has not read yet
+        host = self._host_buffers()
+        self.host_scal, self.host_xvec, self.host_masks = host
         try:
             torch.cuda.synchronize()
             with torch.cuda.stream(side):
                 g.capture_begin()
                 try:
+                    # snapshot of the incoming state (one memcpy node): a replay launched
+                    # ahead of the previous sweep's stop test can be undone
+                    self.state_backup.copy_(self.state)
                     self.timer.begin_capture()
                     self._sweep()
                     self.timer.end_capture()
@@ -922,7 +968,13 @@ class _Engine:
         # (grid.py:60-93 tallies per call)
         self.graph_comm = self.coll.counters.since(comm0)
         self.coll.counters.restore(comm0)
-        return g, self.timer.graph_marks
+        return g, self.timer.graph_marks, host
+
+    def _host_buffers(self):
+        pin = dict(pin_memory=True)
+        return (torch.zeros(2, dtype=torch.float64, **pin),
+                torch.zeros(1 + self.nranks * self.N, dtype=torch.float64, **pin),
+                torch.zeros(2 * self.N, dtype=torch.int32, **pin))
 
     def model_host(self):
         return [h.detach().cpu().numpy() for h in self.owned], self.lam.detach().cpu().numpy()

@@ -228,6 +228,31 @@ def test_cuda_graph_matches_eager(P, golden):
         assert all(sum(row.values()) > 0 for row in graph.rows[1:])
 
 
+@pytest.mark.parametrize("name", ["c1_mu", "hals_r16", "bpp4"])
+def test_graph_run_ahead_stops_where_eager_stops(P, golden, name):
+    """Graph replays run sweep i+1 before sweep i's stop test; a run that converges mid-way
+    (tol = the eager run's eps at iteration 5) must stop at the same iteration with the same
+    model, bitwise: the run-ahead sweep is undone from the replay's own state snapshot."""
+    import dataclasses
+
+    g = golden("runs.npz")
+    _, _, _, _, x, cfg = _run_case(P, g, name, cuda_graph=False)
+    cfg = dataclasses.replace(cfg, max_iters=max(cfg.max_iters, 8), tol=0.0)
+    free = P.nncp_sequential(x, cfg)
+    stop_at = 5
+    tol = free.errors[stop_at]
+    assert min(free.errors[1:stop_at]) > tol, "the trace must first reach tol at iteration 5"
+    runs = [P.nncp_sequential(x, dataclasses.replace(cfg, tol=tol, cuda_graph=graph)) for graph in (False, True)]
+    for rep in runs:
+        assert rep.converged and len(rep.errors) == stop_at + 1, (name, len(rep.errors))
+        assert rep.errors == free.errors[:stop_at + 1]
+    eager, graph = runs
+    assert graph.tree_partial_calls == eager.tree_partial_calls
+    for a, b in zip(eager.model.factors, graph.model.factors):
+        assert np.array_equal(a, b)
+    assert np.array_equal(eager.model.lam, graph.model.lam)
+
+
 @pytest.mark.parametrize("engine", ["fp64", "sliced"])
 def test_pinned_host_input_matches_numpy_and_device_input(P, golden, engine):
     """nncp_sequential on a page-locked host tensor (asynchronous upload, sliced buffer
