@@ -384,6 +384,17 @@ class DistCollectives:
             dist_groups = make_slice_process_groups(grid)
         self.slice_pg = [dist_groups[n][c] for n, c in enumerate(layout.coord)]
 
+    def _padded_rows(self, parts: DistMap, device):
+        """Row k of the concatenated blocks -> its row in the [member][max block] padded
+        layout (cached per partition and device)."""
+        cache = self.__dict__.setdefault("_pad_cache", {})
+        key = (tuple(parts.lengths), str(device))
+        if key not in cache:
+            width = parts.max_length
+            idx = [k * width + i for k in range(parts.parts) for i in range(parts.lengths[k])]
+            cache[key] = torch.tensor(idx, dtype=torch.int64, device=device)
+        return cache[key]
+
     def all_reduce(self, t, op="sum", words=None):
         """``words``: the payload the reference's call carries when ``t`` also carries
         piggy-backed internal words (the status codes on beta's All-Reduce)."""
@@ -411,10 +422,9 @@ class DistCollectives:
             if all(x == width for x in parts.lengths):
                 inp = t.reshape(-1)
             else:
-                inp = torch.zeros((group.size, width, r), dtype=t.dtype, device=t.device)
-                for k in range(group.size):
-                    blk = parts.block(k)
-                    inp[k, : blk.stop - blk.start] = t[blk]
+                # ragged blocks: one scatter into the zero-padded [member][width] layout
+                inp = torch.zeros((group.size * width, r), dtype=t.dtype, device=t.device)
+                inp.index_copy_(0, self._padded_rows(parts, t.device), t)
                 inp = inp.reshape(-1)
             if self.stage and t.is_cuda:
                 out_h = torch.empty((width, r), dtype=t.dtype)
@@ -449,7 +459,8 @@ class DistCollectives:
             else:
                 full = torch.empty((group.size, width, r), dtype=t.dtype, device=t.device)
                 self.dist.all_gather_into_tensor(full.reshape(-1), src.reshape(-1), group=self.slice_pg[mode])
-            res = torch.cat([full[k, : parts.lengths[k]] for k in range(group.size)], dim=0)
+            # drop the padding with one gather (ragged blocks)
+            res = full.reshape(group.size * width, r).index_select(0, self._padded_rows(parts, full.device))
         if out is not None and res is not out:
             out.copy_(res)
             res = out
