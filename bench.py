@@ -117,7 +117,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:  # noqa: BLE001
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines[self.first:]:
             parts = [p.strip() for p in line.split(",")]
@@ -128,11 +128,17 @@ class ClockSampler:
                 smax = float(parts[2])
             except ValueError:
                 continue
+            try:
+                power.append(float(parts[3]))
+            except ValueError:
+                pass
             for name, val in zip(names, parts[5:9]):
                 if val.lower() in ("active", "1"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons),
+                # board power under load: the 2048^3 sweep runs at the 1000 W limit
+                "power_w": statistics.median(power) if power else None}
 
 
 # ------------------------------------------------------------ CPU side ------
