@@ -13,7 +13,7 @@
 
 namespace nncp {
 
-template <int ALGO>
+template <int ALGO, int RP>
 __global__ void __launch_bounds__(kRowWarps * 32)
     update_rows_kernel(const double* __restrict__ grams, int order, int mode, int R,
                        const double* __restrict__ mrows, const double* __restrict__ owned,
@@ -23,10 +23,17 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   __shared__ double S[kMaxRank * kMaxRank];
   __shared__ double red[kRowWarps * 64];
   __shared__ double colbuf[kMaxRank + 1];
+  __shared__ double inv_diag[kMaxRank];
+  constexpr int NH = (RP + 31) / 32;   // column slots per lane
 #ifdef NNCP_UPD_TIMING
   const long long tu0 = clock64();
 #endif
   load_hadamard(S, grams, order, mode, R);
+  __syncthreads();
+  // HALS: 1 / S_rr once per CTA (the same quotient the row loop formed per column,
+  // off the column chain)
+  if (ALGO == NNCP_ALGO_HALS)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) inv_diag[r] = 1.0 / S[r * R + r];
   __syncthreads();
 #ifdef NNCP_UPD_TIMING
   const long long tu1 = clock64();
@@ -41,9 +48,9 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   for (int64_t i = int64_t(blockIdx.x) * kRowWarps + warp; i < rows; i += int64_t(gridDim.x) * kRowWarps) {
     const double* orow = owned + i * R;
     const double* mr = mrows + i * R;
-    double h[2], m[2];
+    double h[2] = {0.0, 0.0}, m[2] = {0.0, 0.0};
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NH; ++q) {
       const int r = lane + 32 * q;
       h[q] = (r < R) ? (lam ? orow[r] * lam[r] : orow[r]) : 0.0;  // driver.py:403 current = owned * lam
       // M row-major, or (mld > 0) the dimension tree's column-major temporary itself
@@ -52,16 +59,18 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     if (ALGO == NNCP_ALGO_MU) {
       // updaters.py:93-94: current * M / (current @ S + eps)
       double d[2] = {0.0, 0.0};
-      for (int cc = 0; cc < R; ++cc) {
+#pragma unroll
+      for (int cc = 0; cc < RP; ++cc) {
+        if (cc >= R) break;
         const double hc = __shfl_sync(0xffffffffu, cc < 32 ? h[0] : h[1], cc & 31);
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NH; ++q) {
           const int r = lane + 32 * q;
           if (r < R) d[q] = fma(hc, S[cc * R + r], d[q]);
         }
       }
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < NH; ++q) {
         const int r = lane + 32 * q;
         h[q] = (r < R) ? h[q] * m[q] / (d[q] + mu_eps) : 0.0;
       }
@@ -79,34 +88,37 @@ __global__ void __launch_bounds__(kRowWarps * 32)
       // correction (the correctly rounded division in all but rare tie cases), the
       // reciprocal formed off the chain.
       double g[2] = {0.0, 0.0};
-      for (int j = 0; j < R; ++j) {
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {
+        if (j >= R) break;
         const double hj = __shfl_sync(0xffffffffu, j < 32 ? h[0] : h[1], j & 31);
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NH; ++q) {
           const int c = lane + 32 * q;
           if (c < R && j >= c) g[q] = fma(hj, S[j * R + c], g[q]);    // sum_{j >= c} h_j S[j][c]
         }
       }
-      for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        if (r >= R) break;
         const double dg = S[r * R + r];
-        const double idg = 1.0 / dg;
+        const double idg = inv_diag[r];
         const int q = r >> 5;
-        double v = 0.0;
-        if ((r & 31) == lane) {
-          v = q ? h[1] : h[0];   // a skipped column (S_rr <= 0) keeps its value
-          if (dg > 0.0) {
-            const double num = (q ? m[1] : m[0]) - (q ? g[1] : g[0]);
-            const double q0 = num * idg;
-            const double quo = fma(fma(-q0, dg, num), idg, q0);
-            const double col = v + quo;
-            v = (col < 0.0) ? 0.0 : col;
-            if (q) h[1] = v; else h[0] = v;
-          }
-        }
+        // every lane evaluates the column step on its own slot, branch-free; lane r % 32's
+        // value is the one broadcast (no divergent region on the column chain)
+        const double hv = q ? h[1] : h[0];
+        const double num = (q ? m[1] : m[0]) - (q ? g[1] : g[0]);
+        const double q0 = num * idg;
+        const double quo = fma(fma(-q0, dg, num), idg, q0);
+        const double col = hv + quo;
+        double v = (dg > 0.0) ? ((col < 0.0) ? 0.0 : col) : hv;   // a skipped column (S_rr <= 0) keeps its value
         v = __shfl_sync(0xffffffffu, v, r & 31);
+        if ((r & 31) == lane) {
+          if (q) h[1] = v; else h[0] = v;
+        }
         if (v != 0.0) {
 #pragma unroll
-          for (int qq = 0; qq < 2; ++qq) {
+          for (int qq = 0; qq < NH; ++qq) {
             const int c = lane + 32 * qq;
             if (c < R && c > r) g[qq] = fma(v, S[r * R + c], g[qq]);
           }
@@ -115,7 +127,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     }
     double* hr = hhat + i * R;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NH; ++q) {
       const int r = lane + 32 * q;
       if (r < R) {
         hr[r] = h[q];
@@ -669,7 +681,8 @@ __global__ void __launch_bounds__(256)
       ib[o] = e - (e / R) * R;
     }
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int il = 0; il < nr; ++il) {
+#pragma unroll 8
+    for (int il = 0; il < nr; ++il) {     // unrolled: the shared loads run ahead of the FMA chains
       const double* tr = tile + il * RP;
 #pragma unroll
       for (int o = 0; o < 4; ++o) s[o] = fma(tr[ia[o]], tr[ib[o]], s[o]);
@@ -889,14 +902,20 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
   if (algo == NNCP_ALGO_MU || algo == NNCP_ALGO_HALS) {
     const int blocks = row_blocks(rows);
     if (w.part_elems < size_t(blocks) * (rank + 1)) return fail(NNCP_ERR_VALUE, "workspace too small (update)");
-    if (algo == NNCP_ALGO_MU)
-      update_rows_kernel<NNCP_ALGO_MU><<<blocks, kRowWarps * 32, 0, st>>>(
-          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps, mld, tl);
-    else
-      update_rows_kernel<NNCP_ALGO_HALS><<<blocks, kRowWarps * 32, 0, st>>>(
-          grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq, beta, status, w.tickets + T_UPDATE,
-          mu_eps, mld, tl);
+    const int rp32 = rank <= 16 ? 16 : rank <= 32 ? 32 : 64;   // unrolled column loops
+    auto launch = [&](auto kern) {
+      kern<<<blocks, kRowWarps * 32, 0, st>>>(grams, order, mode, rank, mrows, owned, lam, rows, hhat, w.part, nsq,
+                                              beta, status, w.tickets + T_UPDATE, mu_eps, mld, tl);
+    };
+    if (algo == NNCP_ALGO_MU) {
+      if (rp32 == 16) launch(update_rows_kernel<NNCP_ALGO_MU, 16>);
+      else if (rp32 == 32) launch(update_rows_kernel<NNCP_ALGO_MU, 32>);
+      else launch(update_rows_kernel<NNCP_ALGO_MU, 64>);
+    } else {
+      if (rp32 == 16) launch(update_rows_kernel<NNCP_ALGO_HALS, 16>);
+      else if (rp32 == 32) launch(update_rows_kernel<NNCP_ALGO_HALS, 32>);
+      else launch(update_rows_kernel<NNCP_ALGO_HALS, 64>);
+    }
   } else if (algo == NNCP_ALGO_BPP) {
     NNCP_RP_CASES(rp, {
       constexpr int NW = bpp_warps<RP>();
