@@ -626,14 +626,24 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 
 // --------------------------------------------------- normalise + Gram ------
 constexpr int kGramRows = 64;
+template <int RP>
+constexpr int gram_rows() {   // rows per normalise+Gram CTA
+  return RP <= 32 ? 128 : kGramRows;
+}
 
 template <int RP>
 __global__ void __launch_bounds__(256)
     normalize_gram_kernel(const double* __restrict__ hhat, const double* __restrict__ nsq, int64_t rows, int R,
                           double* __restrict__ owned, double* __restrict__ lam, double* __restrict__ gram,
                           double* __restrict__ part, unsigned int* ticket, const PublishArgs pub) {
-  __shared__ double tile[kGramRows * RP];
+  // rows per CTA: 128 up to R = 32 (half the per-CTA Gram partials the last CTA sums)
+  constexpr int GR = gram_rows<RP>();
+  __shared__ __align__(16) double tile[GR * RP];
   __shared__ double scale[RP];
+  __shared__ double rscale[RP];
+#ifdef NNCP_UPD_TIMING
+  const long long tn0 = clock64();
+#endif
   if (threadIdx.x < R) {
     double s = 1.0;
     if (nsq) {
@@ -642,13 +652,17 @@ __global__ void __launch_bounds__(256)
       if (blockIdx.x == 0 && lam) lam[threadIdx.x] = w;
     }
     scale[threadIdx.x] = s;
+    rscale[threadIdx.x] = 1.0 / s;
   }
   __syncthreads();
-  const int64_t r0 = int64_t(blockIdx.x) * kGramRows;
-  const int nr = int(rows - r0 < kGramRows ? rows - r0 : int64_t(kGramRows));
+#ifdef NNCP_UPD_TIMING
+  const long long tn1 = clock64();
+#endif
+  const int64_t r0 = int64_t(blockIdx.x) * GR;
+  const int nr = int(rows - r0 < GR ? rows - r0 : int64_t(GR));
   // every load of the tile issued before the first use (a load-use loop serialised
   // PER global-memory latencies; this kernel is latency-bound at these sizes)
-  constexpr int PER = (kGramRows * RP + 255) / 256;
+  constexpr int PER = (GR * RP + 255) / 256;
   double v[PER];
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
@@ -658,41 +672,65 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int e = int(threadIdx.x) + 256 * k, il = e / RP, r = e % RP;
-    if (il < nr && r < R) {
-      double x = v[k];
-      if (nsq) {
-        x = x / scale[r];
+    if (il < nr) {
+      double x = v[k];   // 0 in the padding columns r >= R
+      if (nsq && r < R) {
+        // x / w (driver.py:416-418) as the product with the column's reciprocal plus one
+        // FMA residual correction: the correctly rounded quotient bar rare ties, without
+        // a full division per element (the divisions were most of this kernel's row phase)
+        const double w = scale[r], iw = rscale[r];
+        const double q0 = x * iw;
+        x = fma(fma(-q0, w, x), iw, q0);
         owned[(r0 + il) * R + r] = x;
       }
       tile[il * RP + r] = x;
     }
   }
   __syncthreads();
+#ifdef NNCP_UPD_TIMING
+  const long long tn2 = clock64();
+#endif
   if (gram == nullptr) return;  // row scaling only
   const int RR = R * R;
   double* mypart = part + size_t(blockIdx.x) * RR;
-  // four entries per thread in flight (four independent FMA chains over the rows)
-  for (int e0 = threadIdx.x; e0 < RR; e0 += 4 * blockDim.x) {
-    int ia[4], ib[4];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-      const int e = min(e0 + o * int(blockDim.x), RR - 1);
-      ia[o] = e / R;
-      ib[o] = e - (e / R) * R;
-    }
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+  // 2 x 2 register blocks of G: per row one 16-byte load of the block's two a-values and
+  // one of its two b-values feed four FMA chains (one entry per chain read two 8-byte
+  // words per FMA: shared-memory bound); every entry still sums its rows in order
+  constexpr int NB2 = RP / 2;
+  for (int blk = threadIdx.x; blk < NB2 * NB2; blk += blockDim.x) {
+    const int a0 = 2 * (blk / NB2), b0 = 2 * (blk % NB2);
+    if (a0 >= R || b0 >= R) continue;
+    double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
 #pragma unroll 8
-    for (int il = 0; il < nr; ++il) {     // unrolled: the shared loads run ahead of the FMA chains
-      const double* tr = tile + il * RP;
-#pragma unroll
-      for (int o = 0; o < 4; ++o) s[o] = fma(tr[ia[o]], tr[ib[o]], s[o]);
+    for (int il = 0; il < nr; ++il) {
+      const double2 xa = *reinterpret_cast<const double2*>(tile + il * RP + a0);
+      const double2 xb = *reinterpret_cast<const double2*>(tile + il * RP + b0);
+      s00 = fma(xa.x, xb.x, s00);
+      s01 = fma(xa.x, xb.y, s01);
+      s10 = fma(xa.y, xb.x, s10);
+      s11 = fma(xa.y, xb.y, s11);
     }
-#pragma unroll
-    for (int o = 0; o < 4; ++o)
-      if (e0 + o * int(blockDim.x) < RR) mypart[e0 + o * blockDim.x] = s[o];
+    mypart[a0 * R + b0] = s00;
+    if (b0 + 1 < R) mypart[a0 * R + b0 + 1] = s01;
+    if (a0 + 1 < R) {
+      mypart[(a0 + 1) * R + b0] = s10;
+      if (b0 + 1 < R) mypart[(a0 + 1) * R + b0 + 1] = s11;
+    }
   }
+#ifdef NNCP_UPD_TIMING
+  const long long tn3 = clock64();
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("normalize cta %d/%d: scale %lld rows %lld gram %lld\n", blockIdx.x, gridDim.x, tn1 - tn0, tn2 - tn1,
+           tn3 - tn2);
+#endif
   if (last_cta_ticket(ticket)) {
-    finish_partials(part, gridDim.x, RR, gram);
+#ifdef NNCP_UPD_TIMING
+    const long long tn4 = clock64();
+#endif
+    finish_partials<8>(part, gridDim.x, RR, gram);
+#ifdef NNCP_UPD_TIMING
+    if (threadIdx.x == 0) printf("normalize last cta %d: ticket %lld finish %lld\n", blockIdx.x, tn4 - tn3, clock64() - tn4);
+#endif
     if (pub.gamma != nullptr) {
       // the sweep's last normalisation also produces gamma and hands the status off
       // (a single context: no All-Reduce of the Gram in between) -- one launch fewer
@@ -941,9 +979,10 @@ static int normalize_gram_impl(const double* hhat, const double* nsq, int64_t ro
                    const PublishArgs* pub) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int rp = pad8(rank);
-  const int blocks = int(std::max<int64_t>(1, (rows + kGramRows - 1) / kGramRows));
-  if (gram && w.part_elems < size_t(blocks) * rank * rank) return fail(NNCP_ERR_VALUE, "workspace too small (gram)");
-  NNCP_RP_CASES(rp, (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
+  NNCP_RP_CASES(rp, const int blocks = int(std::max<int64_t>(1, (rows + gram_rows<RP>() - 1) / gram_rows<RP>()));
+                if (gram && w.part_elems < size_t(blocks) * rank * rank)
+                  return fail(NNCP_ERR_VALUE, "workspace too small (gram)");
+                (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
                                                                       owned, lam, gram, w.part,
                                                                       w.tickets + ticket_slot,
                                                                       pub ? *pub : PublishArgs{})));

@@ -98,6 +98,9 @@ static __device__ double block_sum(double v, double* red) {
 // is split into `segs` strided segments with eight accumulators, then the segments
 // are summed in order; otherwise a thread owns four outputs and issues 4 x 4 loads
 // per step.  Deterministic for a given launch configuration.
+// DEPTH: partial blocks in flight per entry when n exceeds the block size (the Gram's
+// R x R entries): each round is one L2 round trip for the last CTA.
+template <int DEPTH = 4>
 static __device__ void finish_partials(const double* part, int nblk, int n, double* out) {
   __shared__ double seg_sum[1024];
   const int T = blockDim.x;
@@ -129,28 +132,34 @@ static __device__ void finish_partials(const double* part, int nblk, int n, doub
     }
   } else {
     for (int e0 = threadIdx.x; e0 < n; e0 += 4 * T) {
-      double a[4][4];
+      double a[4][DEPTH];
 #pragma unroll
       for (int o = 0; o < 4; ++o)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) a[o][q] = 0.0;
-      for (int b = 0; b < nblk; b += 4) {
-        double v[4][4];
+        for (int q = 0; q < DEPTH; ++q) a[o][q] = 0.0;
+      for (int b = 0; b < nblk; b += DEPTH) {
+        double v[4][DEPTH];
 #pragma unroll
         for (int o = 0; o < 4; ++o)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < DEPTH; ++q) {
             const int e = e0 + o * T;
             v[o][q] = (e < n && b + q < nblk) ? part[size_t(b + q) * n + e] : 0.0;
           }
 #pragma unroll
         for (int o = 0; o < 4; ++o)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[o][q] += v[o][q];
+          for (int q = 0; q < DEPTH; ++q) a[o][q] += v[o][q];
       }
 #pragma unroll
-      for (int o = 0; o < 4; ++o)
-        if (e0 + o * T < n) out[e0 + o * T] = (a[o][0] + a[o][1]) + (a[o][2] + a[o][3]);
+      for (int o = 0; o < 4; ++o) {
+        // pairwise, fixed order
+#pragma unroll
+        for (int w = 1; w < DEPTH; w *= 2)
+#pragma unroll
+          for (int q = 0; q + w < DEPTH; q += 2 * w) a[o][q] += a[o][q + w];
+        if (e0 + o * T < n) out[e0 + o * T] = a[o][0];
+      }
     }
   }
 }
