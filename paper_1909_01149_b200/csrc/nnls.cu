@@ -658,8 +658,10 @@ __global__ void __launch_bounds__(256)
 #ifdef NNCP_UPD_TIMING
   const long long tn1 = clock64();
 #endif
-  const int64_t r0 = int64_t(blockIdx.x) * GR;
-  const int nr = int(rows - r0 < GR ? rows - r0 : int64_t(GR));
+  // the launch picks the CTA count (<= GR rows each): few rows -> more, shorter CTAs
+  const int64_t grk = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = int64_t(blockIdx.x) * grk;
+  const int nr = int(rows - r0 < grk ? rows - r0 : grk);   // <= 0: an empty CTA (zero partial)
   // every load of the tile issued before the first use (a load-use loop serialised
   // PER global-memory latencies; this kernel is latency-bound at these sizes)
   constexpr int PER = (GR * RP + 255) / 256;
@@ -979,7 +981,10 @@ static int normalize_gram_impl(const double* hhat, const double* nsq, int64_t ro
                    const PublishArgs* pub) {
   WsLayout w = ws_layout(ws, ws_bytes);
   const int rp = pad8(rank);
-  NNCP_RP_CASES(rp, const int blocks = int(std::max<int64_t>(1, (rows + gram_rows<RP>() - 1) / gram_rows<RP>()));
+  // rows per CTA: 32 up to 512 rows, 64 up to 1024, then the kernel's maximum (measured:
+  // the Gram chain and the partial count trade off)
+  NNCP_RP_CASES(rp, const int64_t gr = std::min<int64_t>(gram_rows<RP>(), rows <= 512 ? 32 : rows <= 1024 ? 64 : 128);
+                const int blocks = int(std::max<int64_t>(1, (rows + gr - 1) / gr));
                 if (gram && w.part_elems < size_t(blocks) * rank * rank)
                   return fail(NNCP_ERR_VALUE, "workspace too small (gram)");
                 (normalize_gram_kernel<RP><<<blocks, 256, 0, st>>>(hhat, nsq, std::max<int64_t>(rows, 0), rank,
