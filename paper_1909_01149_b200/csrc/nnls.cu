@@ -908,7 +908,7 @@ int row_blocks(int64_t rows) {
 size_t row_update_part_elems(int64_t rows, int rank) {
   const int64_t blocks_rows = row_blocks(rows);
   const int64_t blocks_bpp = std::min<int64_t>((rows + kBppWarps - 1) / kBppWarps, int64_t(num_sms()) * 4);
-  const int64_t blocks_gram = (rows + kGramRows - 1) / kGramRows;
+  const int64_t blocks_gram = (rows + 31) / 32;   // normalise+Gram: >= 32 rows per CTA
   size_t e = std::max<int64_t>(blocks_rows, blocks_bpp) * (rank + 6);  // + ADMM/NES step partials
   e = std::max<size_t>(e, size_t(std::max<int64_t>(blocks_gram, 1)) * rank * rank);
   e = std::max<size_t>(e, size_t(num_sms()) * 8 * 4);   // norm_squared(_min): <= 8 blocks/SM, sum + 3 extrema
