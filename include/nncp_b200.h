@@ -180,6 +180,17 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
                    const double* owned, const double* lam, int64_t rows, double* hhat, double* nsq, double* beta,
                    int* status, double mu_eps, void* bpp_sets, int64_t m_ld, void* ws, size_t ws_bytes,
                    void* stream);
+/* BPP's S = prod_{m != mode} sym(G_m) and S^-1 formed ahead of the update -- they need
+ * only the Grams, so a caller can launch this on a second stream while the mode's
+ * MTTKRP runs and join before nncp_update_ex / _grouped / _normalize (driver.py:396-418:
+ * the Gram Hadamard + the solves of updaters.py:121-164).  The result goes into a
+ * block after the passive sets of `bpp_sets` (allocate nncp_bpp_sets_words(rows, rank)
+ * uint64 words instead of rows); the next BPP update of that buffer with the same
+ * (order, mode, rank) takes S and S^-1 from it instead of forming them (the same
+ * bits: it is the update's own elimination) and marks the block used. */
+size_t nncp_bpp_sets_words(int64_t rows, int rank);
+int nncp_bpp_prepare(const double* grams, int order, int mode, int rank, void* bpp_sets, int64_t rows,
+                     void* stream);
 /* nncp_update_ex with M given as m_groups column-major partials (leading dimension
  * m_ld >= rows, m_gstride >= m_ld * rank doubles apart) summed in group order while the
  * rows are loaded -- the output of nncp_partial_mttkrp_sliced_deferred.  MU, HALS, BPP.

@@ -74,6 +74,9 @@ SIGNATURES = [
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp,
       ctypes.c_double, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp,
       ctypes.c_size_t, vp]),
+    ("nncp_bpp_sets_words", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int]),
+    ("nncp_bpp_prepare", ctypes.c_int,
+     [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp]),
     ("nncp_update_grouped", ctypes.c_int,
      [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
       vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_double, vp, vp, ctypes.c_size_t, vp]),

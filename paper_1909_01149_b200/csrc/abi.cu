@@ -40,6 +40,8 @@ int inner(const double*, const double*, const double*, int64_t, int, double*, vo
 int norm_squared(const double*, int64_t, double*, double*, void*, size_t, cudaStream_t);
 int status_reset(int*, int, cudaStream_t);
 size_t row_update_part_elems(int64_t rows, int rank);
+size_t bpp_sets_words(int64_t rows, int rank);
+int bpp_prepare(const double*, int, int, int, void*, int64_t, cudaStream_t);
 int ucp(const double*, int, int, int, const double*, int64_t, double*, double*, double*, int*, void*, size_t,
         cudaStream_t, int64_t, const TailArgs*);
 int admm_step(const double*, int, int, int, double, const double*, const double*, double*, double*, int64_t, double*,
@@ -283,6 +285,14 @@ int nncp_update_ex(int algo, const double* grams, int order, int mode, int rank,
                    void* stream) {
   return update_dispatch(algo, grams, order, mode, rank, mttkrp_rows, owned, lam, rows, hhat, nsq, beta, status, mu_eps,
                          bpp_sets, m_ld, nullptr, ws, ws_bytes, stream);
+}
+
+size_t nncp_bpp_sets_words(int64_t rows, int rank) { return bpp_sets_words(rows, rank); }
+
+int nncp_bpp_prepare(const double* grams, int order, int mode, int rank, void* bpp_sets, int64_t rows, void* stream) {
+  if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
+  if (order > kMaxOrder || mode < 0 || mode >= order) return fail(NNCP_ERR_VALUE, "exclude index out of range");
+  return bpp_prepare(grams, order, mode, rank, bpp_sets, rows, S(stream));
 }
 
 int nncp_update_grouped(int algo, const double* grams, int order, int mode, int rank, const double* mttkrp_parts,

@@ -463,6 +463,42 @@ __device__ bool block_inverse(const double* S, int R, double* aug, double* TT, d
   return true;
 }
 
+// BPP's S and S^-1 prepared ahead of the update (nncp_bpp_prepare, launched on another
+// stream while the mode's MTTKRP runs -- S needs only the Grams): a block after the
+// caller's passive sets, uint64 sets[rows rounded up to 2], then
+//   [0] key (0 = none), [1] t_ok, [2..3] unused, S^T (R x R), S^-1 transposed (R x R).
+// The update takes S and S^-1 from it when the key matches (order, mode, R) and its
+// last CTA clears the key: a block is used at most once.
+__host__ __device__ inline unsigned long long bpp_prep_key(int order, int mode, int R) {
+  return (0x4250ull << 48) | (unsigned long long)(order + 1) << 32 | (unsigned long long)(mode + 1) << 16 |
+         (unsigned long long)R;
+}
+__host__ __device__ inline int64_t bpp_prep_offset(int64_t rows) { return (rows + 1) / 2 * 2; }
+inline size_t bpp_prep_words(int rank) { return 4 + 2 * size_t(rank) * rank; }
+
+template <int RP>
+__global__ void __launch_bounds__(bpp_warps<RP>() * 32)
+    bpp_prepare_kernel(const double* __restrict__ grams, int order, int mode, int R, double* __restrict__ blk) {
+  extern __shared__ __align__(16) double dsm[];
+  double* S = dsm;                 // RP*RP (S^T, as bpp_kernel holds it)
+  double* TT = S + RP * RP;        // RP*RP
+  double* gj = TT + RP * RP;       // 6 RP
+  double* aug = gj + 6 * RP;       // RP * 2 RP
+  load_hadamard<true>(S, grams, order, mode, R);
+  __syncthreads();
+  const bool t_ok = block_inverse<RP>(S, R, aug, TT, gj);   // bpp_kernel's own elimination: the same bits
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    blk[4 + e] = S[e];
+    blk[4 + R * R + e] = TT[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    reinterpret_cast<unsigned long long*>(blk)[1] = t_ok ? 1ull : 0ull;
+    reinterpret_cast<unsigned long long*>(blk)[0] = bpp_prep_key(order, mode, R);
+  }
+}
+
 template <int RP>
 __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
     bpp_kernel(const double* __restrict__ grams, int order, int mode, int R, const double* __restrict__ mrows,
@@ -486,14 +522,29 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 #ifdef NNCP_BPP_TIMING
   const long long tk0 = clock64();
 #endif
-  load_hadamard<true>(S, grams, order, mode, R);   // S^T: the gathers below walk columns across lanes
-  __syncthreads();
+  // S and S^-1 prepared ahead (nncp_bpp_prepare), else formed here
+  unsigned long long* prep = psets != nullptr && order > 0 ? psets + bpp_prep_offset(rows) : nullptr;
+  const bool use_prep = prep != nullptr && prep[0] == bpp_prep_key(order, mode, R);
+  bool t_ok;
+  if (use_prep) {
+    const double* blk = reinterpret_cast<const double*>(prep);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      S[e] = blk[4 + e];
+      TT[e] = blk[4 + R * R + e];
+    }
+    t_ok = prep[1] != 0ull;
+    __syncthreads();
+  }
 #ifdef NNCP_BPP_TIMING
   const long long tk1 = clock64();
 #endif
-  // the block-elimination passes need S^-1; order 0 (an explicit S from bpp_update)
-  // need not be symmetric: solve those directly, like the reference
-  const bool t_ok = order > 0 && block_inverse<RP>(S, R, lu, TT, gj);
+  if (!use_prep) {
+    load_hadamard<true>(S, grams, order, mode, R);   // S^T: the gathers below walk columns across lanes
+    __syncthreads();
+    // the block-elimination passes need S^-1; order 0 (an explicit S from bpp_update)
+    // need not be symmetric: solve those directly, like the reference
+    t_ok = order > 0 && block_inverse<RP>(S, R, lu, TT, gj);
+  }
 #ifdef NNCP_BPP_TIMING
   const long long tk2 = clock64();
 #endif
@@ -616,7 +667,7 @@ __global__ void __launch_bounds__(bpp_warps<RP>() * 32)
 #endif
   __syncthreads();
   tail.scratch = lu;   // the per-warp scratch is dead after the rows
-  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail);
+  colsum_epilogue<NH>(sq2, bsum, R, red, colbuf, part, nsq, beta, ticket, &tail, use_prep ? prep : nullptr);
 #ifdef NNCP_BPP_TIMING
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("bpp cta %d warp %d t_ok %d: hadamard %lld inverse %lld rows %lld epilogue %lld\n", blockIdx.x,
@@ -972,6 +1023,25 @@ int update(int algo, const double* grams, int order, int mode, int rank, const d
   } else {
     return fail(NNCP_ERR_VALUE, "algorithm must be MU, HALS or BPP");
   }
+  NNCP_LAUNCH_CHECK();
+  return NNCP_OK;
+}
+
+size_t bpp_sets_words(int64_t rows, int rank) {
+  return size_t(bpp_prep_offset(std::max<int64_t>(rows, 0))) + bpp_prep_words(rank);
+}
+
+int bpp_prepare(const double* grams, int order, int mode, int rank, void* sets, int64_t rows, cudaStream_t st) {
+  if (order < 1) return fail(NNCP_ERR_VALUE, "bpp_prepare needs the Grams of an order >= 1 tensor");
+  if (sets == nullptr) return fail(NNCP_ERR_VALUE, "bpp_prepare needs the passive-set buffer");
+  double* blk = reinterpret_cast<double*>(static_cast<unsigned long long*>(sets) + bpp_prep_offset(rows));
+  const int rp = pad8(rank);
+  NNCP_RP_CASES(rp, {
+    constexpr int NW = bpp_warps<RP>();
+    const size_t smem = sizeof(double) * (4 * size_t(RP) * RP + 6 * RP);
+    if (int rc = set_max_smem_once<bpp_prepare_kernel<RP>>(int(smem))) return rc;
+    bpp_prepare_kernel<RP><<<1, NW * 32, smem, st>>>(grams, order, mode, rank, blk);
+  });
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
 }

@@ -325,7 +325,7 @@ constexpr int kRowWarps = 8;
 template <int NH>
 __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, double* red /* [nw][64] */,
                                 double* colbuf, double* part, double* nsq, double* beta, unsigned int* ticket,
-                                const TailArgs* tail = nullptr) {
+                                const TailArgs* tail = nullptr, unsigned long long* clear_last = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 #pragma unroll
   for (int q = 0; q < NH; ++q) red[warp * 64 + lane + 32 * q] = sq[q];
@@ -344,6 +344,7 @@ __device__ void colsum_epilogue(const double (&sq)[NH], double bsum, int R, doub
   const int stride = R + 1;
   for (int e = threadIdx.x; e < stride; e += blockDim.x) part[size_t(blockIdx.x) * stride + e] = colbuf[e];
   if (last_cta_ticket(ticket)) {
+    if (clear_last != nullptr && threadIdx.x == 0) *clear_last = 0ull;   // every CTA is past its reads
     finish_partials(part, gridDim.x, stride, colbuf);
     __syncthreads();
     for (int e = threadIdx.x; e < stride; e += blockDim.x) {

@@ -508,7 +508,8 @@ class _Engine:
             parts += [((self.dims[n], R), torch.float64) for n in range(N)]
         parts += [((R,), torch.float64), ((N, R, R), torch.float64)]
         if bpp:
-            parts += [((max(self.n_owned[n], 1),), torch.int64) for n in range(N)]
+            # passive sets, then the block nncp_bpp_prepare fills with S and S^-1
+            parts += [((int(self.lib.nncp_bpp_sets_words(self.n_owned[n], R)),), torch.int64) for n in range(N)]
         self.state, views = _state_arena(parts, dev)
         self.state_backup = torch.empty_like(self.state)
         self.owned = views[:N]
@@ -517,6 +518,10 @@ class _Engine:
         self.lam, self.grams = views[k], views[k + 1]
         self.lam.fill_(1.0)
         self.bpp_sets = views[k + 2:] if bpp else None
+        # BPP: S and S^-1 of mode n need only the Grams, so they are formed on a second
+        # stream while mode n's MTTKRP runs (fork / join events, captured into the graph)
+        # (NNCP_BPP_PREPARE=0: formed inside the update, for A/B measurements)
+        self.prep_stream = torch.cuda.Stream() if bpp and os.environ.get("NNCP_BPP_PREPARE") != "0" else None
         self.host_scal, self.host_xvec, self.host_masks = self._host_buffers()
         # stateful rules (updaters.py:56-68): per-mode ADMM dual / Nesterov centre
         rows_max = max(max(self.n_owned), 1)
@@ -624,6 +629,7 @@ class _Engine:
             mb = self.mbar[: self.dims[n]]
             m_ld = 0
             rows_n = self.n_owned[n]
+            prep_done = self._bpp_prepare(n) if self.prep_stream is not None and rows_n > 0 else None
             fused_tail = in_place and R <= 32 and 1 <= rows_n and rows_n * R * R <= FUSED_TAIL_MAX
             grouped = None
             if in_place:
@@ -643,6 +649,8 @@ class _Engine:
             self.timer.mark("MTTKRP")
             m_owned = self.coll.reduce_scatter(n, mb, self.owned_parts[n])
             self._cmark("ReduceScatter")
+            if prep_done is not None:
+                torch.cuda.current_stream().wait_event(prep_done)   # join: S, S^-1 ready
             last = n == N - 1
             if fused_tail:
                 # small single-context block: the update kernel's last CTA also normalises,
@@ -723,6 +731,19 @@ class _Engine:
         self.host_scal.copy_(self.scal[0:2], non_blocking=True)
         self.host_masks.copy_(self.masks, non_blocking=True)
         self.timer.mark("Error")
+
+    def _bpp_prepare(self, n):
+        """Fork: BPP's S and S^-1 for mode n (nncp_bpp_prepare) on the side stream, after
+        everything queued so far (the Grams of the modes before n); returns the join event."""
+        fork = torch.cuda.Event()
+        fork.record()
+        self.prep_stream.wait_event(fork)
+        with torch.cuda.stream(self.prep_stream):
+            _lib.check(self.lib.nncp_bpp_prepare(_lib.ptr(self.grams), self.N, n, self.R,
+                                                 _lib.ptr(self.bpp_sets[n]), self.n_owned[n], self._st()))
+        done = torch.cuda.Event()
+        done.record(self.prep_stream)
+        return done
 
     def _hook(self, t, op):
         return self.coll.all_reduce(t, op)
