@@ -292,6 +292,7 @@ size_t nncp_bpp_sets_words(int64_t rows, int rank) { return bpp_sets_words(rows,
 int nncp_bpp_prepare(const double* grams, int order, int mode, int rank, void* bpp_sets, int64_t rows, void* stream) {
   if (rank < 1 || rank > kMaxRank) return fail(NNCP_ERR_UNSUPPORTED, "rank must be in [1, 64]");
   if (order > kMaxOrder || mode < 0 || mode >= order) return fail(NNCP_ERR_VALUE, "exclude index out of range");
+  if (rows < 0) return fail(NNCP_ERR_VALUE, "negative row count");
   return bpp_prepare(grams, order, mode, rank, bpp_sets, rows, S(stream));
 }
 

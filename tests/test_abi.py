@@ -35,6 +35,11 @@ def test_pure_host_entry_points():
     assert lib.nncp_choose_split(3, _lib.i64([1446680, 69, 25]), 0, ctypes.byref(out)) == 0 and out.value == 1
     assert lib.nncp_choose_split(3, _lib.i64([2, 2, 100]), 0, ctypes.byref(out)) == 0 and out.value == 2
     assert lib.nncp_workspace_bytes(3, _lib.i64([2048] * 3), 2, 32) > 0
+    # BPP passive sets + the prepared S / S^-1 block: rows rounded up to 2, 4 header words, 2 R^2
+    assert lib.nncp_bpp_sets_words(255, 32) == 256 + 4 + 2 * 32 * 32
+    assert lib.nncp_bpp_sets_words(0, 5) == 4 + 2 * 25
+    assert lib.nncp_bpp_prepare(None, 3, 3, 8, None, 10, None) != 0          # mode out of range
+    assert lib.nncp_bpp_prepare(None, 3, 0, 8, None, -1, None) != 0          # negative rows
 
 
 def test_device_calls_fail_loudly_without_gpu():
