@@ -94,3 +94,34 @@ def test_block_for_another_mode_is_ignored(env):
     out_b, nsq_b, _ = _update(env, g, m, order, 2, r, sets_b, prepare_mode=0)   # S of mode 0: not mode 2's
     assert np.array_equal(out_a, out_b) and np.array_equal(nsq_a, nsq_b)
     assert int(sets_b[off].item()) != 0                   # left for a mode-0 update
+
+
+@pytest.mark.parametrize("graph", [None, False])
+@pytest.mark.parametrize("dims", [(24, 20, 16, 18), (160, 120, 20, 18)])   # fused update tail / separate kernels
+def test_sweeps_with_prepared_inverse_equal_in_update_bitwise(env, graph, dims):
+    """Whole BPP runs (4-way, graph replays or eager sweeps): the side-stream S / S^-1 fork
+    and join change nothing in the result."""
+    import os
+
+    import paper_1909_01149_b200 as P
+
+    rng = np.random.default_rng(11)
+    r = 12
+    hs = [rng.random((d, r)) for d in dims]
+    from oracle import nncp_oracle as O
+
+    x = O.khatri_rao(hs) @ np.ones(r)
+    x = x + 0.02 * np.sqrt(np.mean(x * x)) * np.abs(rng.standard_normal(x.size))
+    reps = []
+    for flag in ("0", "1"):
+        os.environ["NNCP_BPP_PREPARE"] = flag
+        try:
+            reps.append(P.nncp_sequential(P.DenseTensor(dims, x), P.RunConfig(
+                rank=r, algorithm="bpp", max_iters=6, tol=0.0, cuda_graph=graph, mttkrp_kernel="fp64")))
+        finally:
+            os.environ.pop("NNCP_BPP_PREPARE", None)
+    a, b = reps
+    assert a.errors == b.errors
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+    assert np.array_equal(a.model.lam, b.model.lam)
