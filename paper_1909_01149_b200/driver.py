@@ -451,6 +451,10 @@ class _Engine:
         self.report = RunReport()
         self.timer = _EventTimer(timing)
         self._wall0 = time.perf_counter()
+        # capture stream created before the first read-back below: torch's first Stream()
+        # builds its stream pool (~40 ms in a fresh process, measured), which then overlaps
+        # an asynchronous tensor upload instead of following it
+        self.capture_stream = torch.cuda.Stream() if cfg.cuda_graph is not False else None
         # init row (driver.py:338-345): ||X||^2 of the local block, in the same read also
         # min x (negative-entry warning), max |x| and the smallest nonzero |x| -- the facts
         # the "auto" MTTKRP engine choice needs before the tensor is sliced
@@ -534,9 +538,6 @@ class _Engine:
                 self.runner = NesterovRunner(rows_max, R, dev, self.ws)
                 self.nes_prev = [None] * N
         self.graphs = []            # [(CUDA graph of one sweep, its timing marks, its read-back buffers)]
-        # capture stream created up front: torch's first Stream() builds its stream pool
-        # (~14 ms, measured), which here overlaps an asynchronous tensor upload
-        self.capture_stream = torch.cuda.Stream() if cfg.cuda_graph is not False else None
         self.graph_failed = False
         self.graph_kernels = 0      # library kernels captured in the sweep graph
         self.graph_replays = 0

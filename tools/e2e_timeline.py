@@ -2,7 +2,7 @@
 already built, caches emptied): host timestamps and CUDA events at the phase
 boundaries of nncp_sequential, no extra synchronisation between them.
 
-    python tools/e2e_timeline.py 2048x2048x2048 32 20
+    [E2E_REPS=n] python tools/e2e_timeline.py 2048x2048x2048 32 20
 """
 import sys
 import time
@@ -26,36 +26,41 @@ del xd
 torch.cuda.empty_cache()
 torch.cuda.synchronize()
 
-marks = []
+import os  # noqa: E402
 
+for rep in range(int(os.environ.get("E2E_REPS", "1"))):
+    print(f"-- run {rep}")
+    marks = []
 
-def mark(label):
-    e = torch.cuda.Event(enable_timing=True)
-    e.record()
-    marks.append((label, time.perf_counter(), e))
+    def mark(label):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((label, time.perf_counter(), e))
 
-
-cfg = P.RunConfig(rank=R, algorithm="hals", max_iters=steps, tol=0.0)
-x = P.DenseTensor(dims, host)
-mark("start")
-D._reserve_sliced(dims, cfg)
-mark("reserved sliced buffer")
-xdev = x.to_device()
-mark("H2D queued")
-eng = D._Engine(xdev.data, dims, dims, cfg, D.IdentityCollectives(), None, timing=False, warn_negative=True)
-mark("engine built (slicing queued)")
-eng.initialise()
-mark("initialised")
-eng.iterate(1)
-mark("sweep 1 (eager)")
-eng.iterate(1)
-mark("sweep 2 (graphs captured)")
-eng.iterate()
-mark(f"sweeps 3-{steps}")
-owned, lam = eng.model_host()
-mark("model D2H")
-torch.cuda.synchronize()
-t0, e0 = marks[0][1], marks[0][2]
-print(f"{'phase end':30s} {'host ms':>9s} {'GPU ms':>9s}")
-for label, t, e in marks:
-    print(f"{label:30s} {1e3 * (t - t0):9.1f} {e0.elapsed_time(e):9.1f}")
+    cfg = P.RunConfig(rank=R, algorithm="hals", max_iters=steps, tol=0.0)
+    x = P.DenseTensor(dims, host)
+    mark("start")
+    D._reserve_sliced(dims, cfg)
+    mark("reserved sliced buffer")
+    xdev = x.to_device()
+    mark("H2D queued")
+    eng = D._Engine(xdev.data, dims, dims, cfg, D.IdentityCollectives(), None, timing=False, warn_negative=True)
+    mark("engine built (slicing queued)")
+    eng.initialise()
+    mark("initialised")
+    eng.iterate(1)
+    mark("sweep 1 (eager)")
+    eng.iterate(1)
+    mark("sweep 2 (graphs captured)")
+    eng.iterate()
+    mark(f"sweeps 3-{steps}")
+    owned, lam = eng.model_host()
+    mark("model D2H")
+    torch.cuda.synchronize()
+    t0, e0 = marks[0][1], marks[0][2]
+    print(f"{'phase end':30s} {'host ms':>9s} {'GPU ms':>9s}")
+    for label, t, e in marks:
+        print(f"{label:30s} {1e3 * (t - t0):9.1f} {e0.elapsed_time(e):9.1f}")
+    del eng, xdev, x
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
