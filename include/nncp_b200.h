@@ -103,6 +103,16 @@ int nncp_partial_mttkrp(const double* x, int order, const int64_t* dims, int spl
 int nncp_sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels, size_t* bytes);
 int nncp_slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
                       size_t bytes, void* stream);
+/* nncp_slice_tensor in two steps, so a run that slices reads the 8-byte tensor once
+ * before the planes pass instead of twice: nncp_norm_rowmax takes the row maxima
+ * into `sliced` AND, in the same read, nncp_norm_squared_min's outputs (out_sum[0] =
+ * sum x^2, out_min[0..2] = min x, max |x|, min nonzero |x|; the facts the engine
+ * choice needs, driver.py:338-345); nncp_slice_tensor_planes then writes the digit
+ * planes from those row maxima (same bits as nncp_slice_tensor). */
+int nncp_norm_rowmax(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                     size_t bytes, double* out_sum, double* out_min, void* ws, size_t ws_bytes, void* stream);
+int nncp_slice_tensor_planes(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                             size_t bytes, void* stream);
 size_t nncp_sliced_workspace_bytes(int order, const int64_t* dims, int split, int rank, int levels);
 int nncp_partial_mttkrp_sliced(const void* sliced, int order, const int64_t* dims, int split, int side,
                                const double* const* factors, int rank, int levels, double* out, void* ws,

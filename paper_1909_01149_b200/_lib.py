@@ -46,6 +46,10 @@ SIGNATURES = [
       ctypes.c_size_t, vp]),
     ("nncp_sliced_tensor_bytes", ctypes.c_int,
      [ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+    ("nncp_norm_rowmax", ctypes.c_int,
+     [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t, vp, vp, vp, ctypes.c_size_t, vp]),
+    ("nncp_slice_tensor_planes", ctypes.c_int,
+     [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t, vp]),
     ("nncp_slice_tensor", ctypes.c_int,
      [vp, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t, vp]),
     ("nncp_sliced_workspace_bytes", ctypes.c_size_t,

@@ -60,6 +60,9 @@ size_t sliced_tensor_bytes(int order, const int64_t* dims, int split, int levels
 size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int levels);
 bool sliced_trailing_supported(int order, const int64_t* dims, int split, int rank, int levels);
 int slice_tensor(const double*, int, const int64_t*, int, int, void*, size_t, cudaStream_t);
+int norm_rowmax(const double*, int, const int64_t*, int, int, void*, size_t, double*, double*, void*, size_t,
+                cudaStream_t);
+int slice_tensor_planes(const double*, int, const int64_t*, int, int, void*, size_t, cudaStream_t);
 int sliced_partial_mttkrp(const void*, int, const int64_t*, int, int, const double* const*, int, int, double*, double*,
                           void*, size_t, cudaStream_t, const double** parts_out = nullptr, int* groups_out = nullptr,
                           int64_t* gstride_out = nullptr);
@@ -163,6 +166,28 @@ int nncp_slice_tensor(const double* x, int order, const int64_t* dims, int split
   size_t avail = 0;
   void* base = align1k(sliced, bytes, &avail);
   return slice_tensor(x, order, dims, split, levels, base, avail, S(stream));
+}
+
+int nncp_norm_rowmax(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                     size_t bytes, double* out_sum, double* out_min, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_common(order, dims, 1);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (!x || !sliced) return fail(NNCP_ERR_VALUE, "null tensor or sliced buffer");
+  size_t avail = 0;
+  void* base = align1k(sliced, bytes, &avail);
+  return norm_rowmax(x, order, dims, split, levels, base, avail, out_sum, out_min, ws, ws_bytes, S(stream));
+}
+
+int nncp_slice_tensor_planes(const double* x, int order, const int64_t* dims, int split, int levels, void* sliced,
+                             size_t bytes, void* stream) {
+  int rc = check_common(order, dims, 1);
+  if (rc) return rc;
+  if (split < 1 || split >= order) return fail(NNCP_ERR_VALUE, "split must be in [1, order-1]");
+  if (!x || !sliced) return fail(NNCP_ERR_VALUE, "null tensor or sliced buffer");
+  size_t avail = 0;
+  void* base = align1k(sliced, bytes, &avail);
+  return slice_tensor_planes(x, order, dims, split, levels, base, avail, S(stream));
 }
 
 size_t nncp_sliced_workspace_bytes(int order, const int64_t* dims, int split, int rank, int levels) {

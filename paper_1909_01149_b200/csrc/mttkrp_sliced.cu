@@ -42,7 +42,7 @@
 //               mbarriers: stage release and accumulator-ready);
 //   warps 2..5  epilogue: tcgen05.ld of the level accumulators (double-buffered in
 //               TMEM when 2 L RP <= 512 columns), fp64 conversion, output stores.
-#include "common.cuh"
+#include "nnls_common.cuh"
 
 namespace nncp {
 namespace sliced {
@@ -168,6 +168,94 @@ __global__ void slice_rowmax_kernel(const double* __restrict__ x, int64_t M, int
   for (; j < j1; ++j) v0 = fmax(v0, fabs(__ldg(p + j * M)));
   const double v = fmax(fmax(v0, v1), fmax(v2, v3));
   atomicMax(rmax + m, (unsigned long long)__double_as_longlong(v));
+}
+
+// slice_rowmax_kernel plus the engine's init-row facts in the same read of X
+// (nncp_norm_squared_min's outputs: sum x^2, min x, max |x|, min nonzero |x|), so a
+// run that slices reads the 8-byte tensor once before the planes pass instead of
+// twice.  Per-CTA partials [4][ctas], summed / min-maxed in CTA order by the last.
+__global__ void __launch_bounds__(256) norm_rowmax_kernel(const double* __restrict__ x, int64_t M, int64_t J,
+                                                          int64_t jper, unsigned long long* __restrict__ rmax,
+                                                          double* __restrict__ part, double* out, double* out_min,
+                                                          unsigned int* ticket) {
+  __shared__ double red[8];
+  __shared__ double redm[3][8];
+  const int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  double s0 = 0.0, s1 = 0.0, mn = INFINITY, a0 = 0.0, a1 = 0.0, anz = INFINITY;
+  bool nonfinite = false;
+  if (m < M) {
+    const int64_t j0 = int64_t(blockIdx.y) * jper;
+    const int64_t j1 = min(J, j0 + jper);
+    const double* p = x + m;
+    int64_t j = j0;
+    for (; j + 2 <= j1; j += 2) {
+      const double u = __ldcs(p + j * M), v = __ldcs(p + (j + 1) * M);
+      s0 = fma(u, u, s0);
+      s1 = fma(v, v, s1);
+      mn = fmin(mn, fmin(u, v));
+      const double au = fabs(u), av = fabs(v);
+      a0 = fmax(a0, au);
+      a1 = fmax(a1, av);
+      anz = fmin(anz, fmin(au > 0.0 ? au : INFINITY, av > 0.0 ? av : INFINITY));
+      nonfinite |= !isfinite(u) || !isfinite(v);
+    }
+    if (j < j1) {
+      const double u = __ldcs(p + j * M), au = fabs(u);
+      s0 = fma(u, u, s0);
+      mn = fmin(mn, u);
+      a0 = fmax(a0, au);
+      anz = fmin(anz, au > 0.0 ? au : INFINITY);
+      nonfinite |= !isfinite(u);
+    }
+    atomicMax(rmax + m, (unsigned long long)__double_as_longlong(fmax(a0, a1)));   // NaN dropped, as before
+  }
+  const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+  const double s = block_sum(s0 + s1, red);
+  if (threadIdx.x == 0) part[bid] = s;
+  double amax = fmax(a0, a1);
+  bool bad = nonfinite;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    anz = fmin(anz, __shfl_xor_sync(0xffffffffu, anz, o));
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    redm[0][threadIdx.x >> 5] = mn;
+    redm[1][threadIdx.x >> 5] = bad ? NAN : amax;
+    redm[2][threadIdx.x >> 5] = anz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = redm[0][0], a = redm[1][0], z = redm[2][0];
+    bool nan = isnan(a);
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+      mm = fmin(mm, redm[0][w]);
+      nan |= isnan(redm[1][w]);
+      a = fmax(a, redm[1][w]);
+      z = fmin(z, redm[2][w]);
+    }
+    part[nb + bid] = mm;
+    part[2 * nb + bid] = nan ? NAN : a;
+    part[3 * nb + bid] = z;
+  }
+  if (last_cta_ticket(ticket)) {
+    finish_partials(part, int(nb), 1, out);
+    if (threadIdx.x == 0) {
+      double mm = part[nb], a = part[2 * nb], z = part[3 * nb];
+      bool nan = isnan(a);
+      for (unsigned b = 1; b < nb; ++b) {
+        mm = fmin(mm, part[nb + b]);
+        nan |= isnan(part[2 * nb + b]);
+        a = fmax(a, part[2 * nb + b]);
+        z = fmin(z, part[3 * nb + b]);
+      }
+      out_min[0] = mm;
+      out_min[1] = nan ? NAN : a;
+      out_min[2] = z;
+    }
+  }
 }
 
 // Thread: 16 consecutive rows m at every column j of its range (padding rows /
@@ -1266,8 +1354,12 @@ size_t sliced_ws_bytes(int order, const int64_t* dims, int split, int rank, int 
   return std::max(l.ws_bytes, r.ws_bytes);
 }
 
-int slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* out, size_t bytes,
-                 cudaStream_t st) {
+// mode 0: row maxima + planes (nncp_slice_tensor); 1: row maxima with the init-row
+// facts (nncp_norm_rowmax); 2: planes from row maxima already in the buffer
+// (nncp_slice_tensor_planes)
+static int slice_tensor_impl(const double* x, int order, const int64_t* dims, int split, int levels, void* out,
+                             size_t bytes, cudaStream_t st, int mode, double* norm_out, double* min_out, void* ws,
+                             size_t ws_bytes) {
   using namespace sliced;
   if (int rc = check_levels(levels)) return rc;
   const TensorLayout t = tensor_layout(order, dims, split, levels);
@@ -1279,14 +1371,26 @@ int slice_tensor(const double* x, int order, const int64_t* dims, int split, int
   int* rowexp = reinterpret_cast<int*>(base);
   int8_t* planes = reinterpret_cast<int8_t*>(base + t.plane_off);
   unsigned long long* rmax = reinterpret_cast<unsigned long long*>(base + t.rmax_off);
-  NNCP_CUDA_TRY(cudaMemsetAsync(rmax, 0, size_t(t.Mp) * 8, st));
   const int64_t target = int64_t(num_sms()) * 16;
-  const int64_t mblocks = (t.M + 255) / 256;
-  int64_t jsplit = std::max<int64_t>(1, std::min<int64_t>(t.J, (target + mblocks - 1) / mblocks));
-  int64_t jper = (t.J + jsplit - 1) / jsplit;
-  jsplit = (t.J + jper - 1) / jper;
-  slice_rowmax_kernel<<<dim3(unsigned(mblocks), unsigned(jsplit)), 256, 0, st>>>(x, t.M, t.J, jper, rmax);
-  NNCP_LAUNCH_CHECK();
+  if (mode != 2) {
+    NNCP_CUDA_TRY(cudaMemsetAsync(rmax, 0, size_t(t.Mp) * 8, st));
+    const int64_t mblocks = (t.M + 255) / 256;
+    int64_t jsplit = std::max<int64_t>(1, std::min<int64_t>(t.J, (target + mblocks - 1) / mblocks));
+    int64_t jper = (t.J + jsplit - 1) / jsplit;
+    jsplit = (t.J + jper - 1) / jper;
+    if (mode == 1) {
+      if (!norm_out || !min_out) return fail(NNCP_ERR_VALUE, "norm outputs required");
+      if (t.M * t.J < 1) return fail(NNCP_ERR_VALUE, "min of an empty tensor");
+      WsLayout w = ws_layout(ws, ws_bytes);
+      if (w.part_elems < size_t(mblocks * jsplit) * 4) return fail(NNCP_ERR_VALUE, "workspace too small (norm)");
+      norm_rowmax_kernel<<<dim3(unsigned(mblocks), unsigned(jsplit)), 256, 0, st>>>(
+          x, t.M, t.J, jper, rmax, w.part, norm_out, min_out, w.tickets + T_NORM);
+      NNCP_LAUNCH_CHECK();
+      return NNCP_OK;
+    }
+    slice_rowmax_kernel<<<dim3(unsigned(mblocks), unsigned(jsplit)), 256, 0, st>>>(x, t.M, t.J, jper, rmax);
+    NNCP_LAUNCH_CHECK();
+  }
   const int64_t gblocks = (t.Mp / 16 + 255) / 256;
   int64_t js2 = std::max<int64_t>(1, std::min<int64_t>(t.Jp, (target + gblocks - 1) / gblocks));
   int64_t jper2 = (t.Jp + js2 - 1) / js2;
@@ -1303,6 +1407,21 @@ int slice_tensor(const double* x, int order, const int64_t* dims, int split, int
 #undef NNCP_SLICE_LAUNCH
   NNCP_LAUNCH_CHECK();
   return NNCP_OK;
+}
+
+int slice_tensor(const double* x, int order, const int64_t* dims, int split, int levels, void* out, size_t bytes,
+                 cudaStream_t st) {
+  return slice_tensor_impl(x, order, dims, split, levels, out, bytes, st, 0, nullptr, nullptr, nullptr, 0);
+}
+
+int norm_rowmax(const double* x, int order, const int64_t* dims, int split, int levels, void* out, size_t bytes,
+                double* norm_out, double* min_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return slice_tensor_impl(x, order, dims, split, levels, out, bytes, st, 1, norm_out, min_out, ws, ws_bytes);
+}
+
+int slice_tensor_planes(const double* x, int order, const int64_t* dims, int split, int levels, void* out,
+                        size_t bytes, cudaStream_t st) {
+  return slice_tensor_impl(x, order, dims, split, levels, out, bytes, st, 2, nullptr, nullptr, nullptr, 0);
 }
 
 int sliced_partial_mttkrp(const void* sliced_x, int order, const int64_t* dims, int split, int side,

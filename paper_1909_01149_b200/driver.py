@@ -461,17 +461,32 @@ class _Engine:
         self.scal = torch.zeros(7, **f64)     # beta, gamma, alpha, beta0, min x, max |x|, min nonzero |x|
         self.timer.start()
         norm_ws = Workspace(1 << 20)
-        _lib.check(self.lib.nncp_norm_squared_min(_lib.ptr(x_local), x_local.numel(),
-                                                  _lib.vp(self.scal.data_ptr() + 16),
-                                                  _lib.vp(self.scal.data_ptr() + 32), norm_ws.ptr, norm_ws.nbytes,
-                                                  _lib.stream_handle()))
+        # when the cost model would slice this tensor, the row maxima of the slicing come
+        # out of the same read of X as the facts (nncp_norm_rowmax; the planes follow
+        # once the facts allow slicing), else the plain norm pass
+        plan0, may_slice = _engine_plan(self.dims, cfg, dev)
+        pre = None
+        if may_slice and x_local.numel() > 0 and cfg.algorithm != "ucp":
+            pre = SlicedTensor(x_local, self.dims, plan0.split, cfg.mttkrp_levels, defer=True)
+            pre.norm_rowmax(x_local, _lib.vp(self.scal.data_ptr() + 16), _lib.vp(self.scal.data_ptr() + 32), norm_ws)
+        else:
+            _lib.check(self.lib.nncp_norm_squared_min(_lib.ptr(x_local), x_local.numel(),
+                                                      _lib.vp(self.scal.data_ptr() + 16),
+                                                      _lib.vp(self.scal.data_ptr() + 32), norm_ws.ptr,
+                                                      norm_ws.nbytes, _lib.stream_handle()))
         self.timer.mark("Error")
         sc = self.scal.tolist()
         self.facts = TensorFacts(sc[2], sc[4], sc[5], sc[6])
-        self.plan, use_sliced = _engine_plan(self.dims, cfg, dev, facts=self.facts)
+        # (the buffer already held counts as available memory)
+        held = pre.buf.numel() if pre is not None else 0
+        self.plan, use_sliced = _engine_plan(self.dims, cfg, dev, extra_bytes=-held, facts=self.facts)
         self.sliced = None
-        if use_sliced:
+        if use_sliced and pre is not None and pre.split == self.plan.split:
+            pre.finish_planes(x_local)
+            self.sliced = pre
+        elif use_sliced:
             self.sliced = SlicedTensor(x_local, self.dims, self.plan.split, cfg.mttkrp_levels)
+        del pre
         ws_bytes = self.plan.workspace_bytes()
         if self.sliced is not None:
             ws_bytes = max(ws_bytes, self.plan.sliced_workspace_bytes(self.sliced.levels))
