@@ -258,49 +258,60 @@ __global__ void __launch_bounds__(256) norm_rowmax_kernel(const double* __restri
   }
 }
 
-// Thread: 16 consecutive rows m at every column j of its range (padding rows /
-// columns written as zeros); 16 bytes per plane into the blocked layout.
+// Thread: PR = 8 consecutive rows m at every column j of its range (padding rows /
+// columns written as zeros); 8 bytes per plane into the blocked layout.  Measured at
+// 2048^3 (tools/slice_timing.py): 16 rows per thread held ~200 registers, one CTA per
+// SM, 25.8 ms; 8 rows, two CTAs, 21.4 ms; 4 rows, three CTAs, 22.9 ms.
+constexpr int PR = 8;
 template <int L, bool VEC>
-__global__ void __launch_bounds__(256) slice_planes_kernel(const double* __restrict__ x, int64_t M, int64_t J,
-                                                           int64_t Mp, int64_t Jp, int64_t njb, int64_t jper,
-                                                           const unsigned long long* __restrict__ rmax,
-                                                           int* __restrict__ rowexp, int8_t* __restrict__ planes) {
-  const int64_t m0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
+__global__ void __launch_bounds__(256, 2) slice_planes_kernel(const double* __restrict__ x, int64_t M, int64_t J,
+                                                              int64_t Mp, int64_t Jp, int64_t njb, int64_t jper,
+                                                              const unsigned long long* __restrict__ rmax,
+                                                              int* __restrict__ rowexp, int8_t* __restrict__ planes) {
+  const int64_t m0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * PR;
   if (m0 >= Mp) return;
-  int ex[16];
+  int ex[PR];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) ex[i] = (m0 + i < M) ? exp_of_bits(rmax[m0 + i]) : 0;
+  for (int i = 0; i < PR; ++i) ex[i] = (m0 + i < M) ? exp_of_bits(rmax[m0 + i]) : 0;
   if (blockIdx.y == 0) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) rowexp[m0 + i] = ex[i];
+    for (int i = 0; i < PR; ++i) rowexp[m0 + i] = ex[i];
   }
   const int64_t mb = m0 / BM;
   const int64_t j0 = int64_t(blockIdx.y) * jper;
   const int64_t j1 = min(Jp, j0 + jper);
-  // the 16 rows' scalings 2^(8L-2-ex) are fixed for the whole column range: test their
+  // column j + 1's values are loaded before column j is sliced
+  auto load = [&](int64_t j, double (&v)[PR]) {
+    const double* src = x + M * j + m0;
+    if (j >= J) {
+#pragma unroll
+      for (int i = 0; i < PR; ++i) v[i] = 0.0;
+    } else if (VEC && m0 + PR <= M) {
+#pragma unroll
+      for (int i = 0; i < PR / 2; ++i) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(src) + i);
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PR; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
+    }
+  };
+  // the rows' scalings 2^(8L-2-ex) are fixed for the whole column range: test their
   // range once (scale_halves' per-element select kept its scalbn path in the issue
   // stream); both arms compute exactly what scale_halves does
   auto sweep = [&](auto scale) {
+    double vn[PR];
+    if (j0 < j1) load(j0, vn);
     for (int64_t j = j0; j < j1; ++j) {
-      double v[16];
-      const double* src = x + M * j + m0;
-      if (j >= J) {
+      double v[PR];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.0;
-      } else if (VEC && m0 + 16 <= M) {
+      for (int i = 0; i < PR; ++i) v[i] = vn[i];
+      if (j + 1 < j1) load(j + 1, vn);
+      uint32_t w[PR / 4][L];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const double2 t = __ldcs(reinterpret_cast<const double2*>(src) + i);
-          v[2 * i] = t.x;
-          v[2 * i + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = (m0 + i < M) ? __ldcs(src + i) : 0.0;
-      }
-      uint32_t w[4][L];
-#pragma unroll
-      for (int g4 = 0; g4 < 4; ++g4) {
+      for (int g4 = 0; g4 < PR / 4; ++g4) {
         int lo[4], hi[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) slice_halves<L>(scale(v[4 * g4 + i], 4 * g4 + i), lo[i], hi[i]);
@@ -308,13 +319,17 @@ __global__ void __launch_bounds__(256) slice_planes_kernel(const double* __restr
       }
       int8_t* blk = planes + ((mb * njb + j / BK) * L) * int64_t(TILE) + (j % BK) * BM + (m0 % BM);
 #pragma unroll
-      for (int s = 0; s < L; ++s)
-        *reinterpret_cast<uint4*>(blk + int64_t(s) * TILE) = make_uint4(w[0][s], w[1][s], w[2][s], w[3][s]);
+      for (int s = 0; s < L; ++s) {
+        if constexpr (PR == 8)
+          *reinterpret_cast<uint2*>(blk + int64_t(s) * TILE) = make_uint2(w[0][s], w[1][s]);
+        else
+          *reinterpret_cast<uint32_t*>(blk + int64_t(s) * TILE) = w[0][s];
+      }
     }
   };
   bool fast = true;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) fast = fast && (8 * L - 2 - ex[i] >= -1022) && (8 * L - 2 - ex[i] <= 1023);
+  for (int i = 0; i < PR; ++i) fast = fast && (8 * L - 2 - ex[i] >= -1022) && (8 * L - 2 - ex[i] <= 1023);
   if (fast) {
     sweep([&ex](double v, int i) { return v * __longlong_as_double((long long)(8 * L - 2 - ex[i] + 1023) << 52); });
   } else {
@@ -1391,7 +1406,7 @@ static int slice_tensor_impl(const double* x, int order, const int64_t* dims, in
     slice_rowmax_kernel<<<dim3(unsigned(mblocks), unsigned(jsplit)), 256, 0, st>>>(x, t.M, t.J, jper, rmax);
     NNCP_LAUNCH_CHECK();
   }
-  const int64_t gblocks = (t.Mp / 16 + 255) / 256;
+  const int64_t gblocks = (t.Mp / PR + 255) / 256;
   int64_t js2 = std::max<int64_t>(1, std::min<int64_t>(t.Jp, (target + gblocks - 1) / gblocks));
   int64_t jper2 = (t.Jp + js2 - 1) / js2;
   js2 = (t.Jp + jper2 - 1) / jper2;
